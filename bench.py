@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark: GUp/s of FDK back-projection on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--mode exact|fast]
+    python bench.py --impl reference ...       # the reference's CPU implementation
+
+Workload (N=1): BASELINE config 2 -- 512^3 float32 volume at 0.5 mm, 496
+filtered projections of 1248x960 (seeded synthetic stand-in for RabbitCT,
+see paper_1401_3615_b200/synth.py), full-basis voxel updates L^3 * N.
+
+One step = one full reconstruction: zero the volume, pack the 496 resident
+projections into the gather layout, back-project them in batches of 32.
+  value : inputs resident in HBM; device-timed with CUDA events; max over ranks.
+  e2e   : the public host API (cbb_reconstruct through reconstruct_arrays) from
+          pinned host projections to the host volume, H2D + kernels + D2H.
+Inputs (2.4 GB raw + 9.6 GB packed) exceed the 126 MB L2, so no flush is needed.
+Multi-GPU (torchrun): each rank owns a z-slab of the same volume (strong
+scaling); no data-path collective in `value`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "oracle")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+METRIC = "GUp/s FDK backprojection, 512^3 & 1024^3 vol, 496x1248x960 proj, 1-8 B200"
+OPS_PER_UPDATE = 34  # algorithmic FP32 ops per voxel update
+GATHER_BYTES_PER_UPDATE = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU seconds for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+# reference arm / CPU baseline: the reference's own reconstruct_optimized
+# (proj/src/kernel_opt.cpp:658-716) built from /root/reference into oracle/_ref
+# ---------------------------------------------------------------------------------
+
+def cpu_inputs(cfg, count):
+    import torch
+
+    from paper_1401_3615_b200 import synth
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g, mats, imgs = synth.make_inputs(cfg, device=dev, out_device="cpu", chunk=16, count=count)
+    return g, mats, imgs.numpy()
+
+
+def time_reference_cpu(cfg, count, g=None, mats=None, imgs=None):
+    """One bounded sample: reconstruct_optimized with the reference defaults
+    (lanes 16, chunk 262, clip + pad, all host threads; CONEBEAM_THREADS honoured)
+    over the first `count` projections into the full config volume. Returns
+    (GUp/s on the full basis from kernel_seconds, stats dict, kind, cores)."""
+    import numpy as np
+
+    import oracle as O
+
+    if g is None:
+        g, mats, imgs = cpu_inputs(cfg, count)
+    L = g.edge_voxels
+    vol = np.zeros((L, L, L), np.float32)
+    cores = os.cpu_count() or 1
+    env_threads = os.environ.get("CONEBEAM_THREADS")
+    if env_threads and env_threads.isdigit() and int(env_threads) > 0:
+        cores = int(env_threads)
+    if O.ref_available():
+        st = O.ref_reconstruct_optimized(vol, g, imgs[:count], mats[:count], workers=cores)
+        if st["status"] != 0:
+            raise RuntimeError("reference reconstruct_optimized failed")
+        kind = "reference"
+        secs = st["kernel_seconds"]
+    else:  # reference not compiled here: the oracle port (bit-exact restatement)
+        t0 = time.perf_counter()
+        O.reconstruct(vol, g, imgs[:count], mats[:count], threads=cores)
+        secs = time.perf_counter() - t0
+        st = {"kernel_seconds": secs, "precompute_seconds": 0.0}
+        kind = "port"
+    gups = L ** 3 * count / secs / 1e9
+    return gups, st, kind, cores
+
+
+def size_cpu_sample(cfg, target_s, max_count=None):
+    """Picks a projection count whose reference CPU run takes ~target_s."""
+    probe = 2
+    g, mats, imgs = cpu_inputs(cfg, probe)
+    gups, st, kind, cores = time_reference_cpu(cfg, probe, g, mats, imgs)
+    per_proj = st["kernel_seconds"] / probe
+    n = int(max(1, min(cfg.num_projections, round(target_s / max(per_proj, 1e-6)))))
+    if max_count:
+        n = min(n, max_count)
+    return n, cores
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1401_3615_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    total_steps = args.steps + args.warmup
+    budget = 150.0  # seconds for the whole run
+    n, cores = size_cpu_sample(cfg, budget / max(total_steps, 1))
+    g, mats, imgs = cpu_inputs(cfg, n)
+    vals, secs = [], []
+    kind = "port"
+    for i in range(total_steps):
+        gups, st, kind, cores = time_reference_cpu(cfg, n, g, mats, imgs)
+        if i >= args.warmup:
+            vals.append(gups)
+            secs.append(st["kernel_seconds"])
+    value = statistics.median(vals)
+    sample = (f"config {args.config} volume {cfg.edge_voxels}^3 x first {n} of "
+              f"{cfg.num_projections} projections per step; reconstruct_optimized defaults "
+              f"(lanes 16, chunk 262, clip+pad), kernel_seconds; full-basis updates")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GUp/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.median(secs), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "edge_voxels": cfg.edge_voxels,
+                   "projections": cfg.num_projections, "detector": [cfg.width, cfg.height],
+                   "sampled_projections": n, "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GUp/s", "cores": cores,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GUp/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1401_3615_b200 as pkg
+    from paper_1401_3615_b200 import synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE {world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = synth.CONFIGS[args.config]
+    mode = pkg.MODE_EXACT if args.mode == "exact" else pkg.MODE_FAST
+    opt = pkg.Options(batch=args.batch, mode=mode)
+    g, mats, imgs = synth.make_inputs(cfg, device=dev, chunk=16)
+    L = g.edge_voxels
+    n, H, W = imgs.shape
+    z0, z1 = L * rank // world, L * (rank + 1) // world
+    _, _, nb = pkg.packed_layout(W, H)
+    packed = torch.empty(n * nb, dtype=torch.uint8, device=dev)
+    vol = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    nbatch = (n + args.batch - 1) // args.batch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(i=None):
+        vol.zero_()
+        if i is not None:
+            ev[i][0].record(stream)
+        pkg.pack_device(imgs, packed, stream)
+        if i is not None:
+            ev[i][1].record(stream)
+        pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream)
+        if i is not None:
+            ev[i][2].record(stream)
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        step()
+    torch.cuda.synchronize()
+    if int(err.item()) != 0:
+        raise RuntimeError("w == 0 hit during warm-up")
+
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches0 = pkg.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = pkg.launch_count() - launches0
+    clocks = sampler.stop()
+    if dist:
+        dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    bp_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)]
+    pack_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)]
+    if dist:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    total_updates = L ** 3 * n  # all ranks together
+    value = total_updates / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (bp_kernel), per launch
+    bp_launch_ms = statistics.mean(bp_ms) / nbatch
+    updates_per_launch = (z1 - z0) * L * L * args.batch
+    peaks, peak_src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lane-ops/s (Tops) at max clock
+    achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
+    sm_load = clocks.get("sm_mhz") or sm_max
+    hbm_bytes = 8 * (z1 - z0) * L * L + args.batch * nb  # volume rmw + packed inputs
+    roofline = {
+        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 3),
+        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
+        "peak_basis": f"{nsm} SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, "
+                      f"{peak_src} peaks file); 34 algorithmic FP32 ops per voxel update",
+        "frac_at_load_clock": round(achieved / (nsm * 128 * sm_load * 1e6 / 1e12), 4),
+        "gups_per_launch": round(updates_per_launch / (bp_launch_ms * 1e-3) / 1e9, 2),
+        "launch_ms": round(bp_launch_ms, 4),
+        "alongside": {
+            "gather": {"achieved_GBps": round(updates_per_launch * GATHER_BYTES_PER_UPDATE /
+                                              (bp_launch_ms * 1e-3) / 1e9, 1),
+                       "peak_GBps": round(nsm * 128 * sm_max * 1e6 / 1e9, 1),
+                       "unit": "L1 B/s (128 B/clk/SM)"},
+            "hbm": {"algorithmic_GBps": round(hbm_bytes / (bp_launch_ms * 1e-3) / 1e9, 1),
+                    "peak_GBps": peaks.get("hbm_gbs")},
+        },
+    }
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GUp/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded ellipsoid phantom + Shepp-Logan ramp filter)",
+        "config": {"workload": cfg.name, "edge_voxels": L, "voxel_mm": cfg.voxel_mm,
+                   "projections": n, "detector": [W, H], "mode": args.mode,
+                   "batch": args.batch, "parallelism": f"z-slab x{world}",
+                   "l2": "inputs larger than L2 (2.4 GB raw + 9.6 GB packed), no flush"},
+        "pack_ms_per_step": round(statistics.mean(pack_ms), 4),
+        "backproject_ms_per_step": round(statistics.mean(bp_ms), 4),
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": roofline,
+    }
+
+    # e2e through the public host API: pinned host projections -> host volume
+    if not args.no_e2e:
+        imgs_h = imgs.cpu().pin_memory()
+        del packed
+        torch.cuda.empty_cache()
+        imgs_np = imgs_h.numpy()
+        vol_h = torch.zeros(((z1 - z0), L, L), dtype=torch.float32).pin_memory()
+        full = np.zeros((L, L, L), np.float32) if world == 1 else None
+        e2e_opt = pkg.Options(batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
+                              volume_is_zero=True, slab=(z0, z1))
+        buf = full if full is not None else np.zeros((L, L, L), np.float32)
+        for _ in range(1):
+            pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)
+        if dist:
+            dist.barrier()
+        e2e_s = []
+        stats = None
+        for _ in range(max(1, min(args.steps, 3))):
+            buf[z0:z1] = 0.0
+            t0 = time.perf_counter()
+            stats = pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)
+            e2e_s.append(time.perf_counter() - t0)
+        e2e_t = statistics.median(e2e_s)
+        if dist:
+            t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        line["e2e"] = {"value": round(total_updates / e2e_t / 1e9, 3), "unit": "GUp/s",
+                       "h2d_bytes_per_step": int(imgs_h.numel() * 4 + mats.nbytes),
+                       "d2h_bytes_per_step": int((z1 - z0) * L * L * 4),
+                       "seconds": round(e2e_t, 4),
+                       "phases": {k: round(v, 4) if isinstance(v, float) else v
+                                  for k, v in stats.items() if k != "per_gpu_kernel_seconds"}}
+        del vol_h
+
+    # CPU baseline: the reference's CPU path on this box's host cores (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cnt, cores = size_cpu_sample(cfg, args.cpu_seconds)
+            gcpu, mcpu, icpu = (g, mats[:cnt], imgs[:cnt].cpu().numpy())
+            gups, st, kind, cores = time_reference_cpu(cfg, cnt, gcpu, mcpu, icpu)
+            line["cpu_baseline"] = {
+                "value": round(gups, 4), "unit": "GUp/s", "cores": cores, "kind": kind,
+                "sample": (f"{L}^3 volume x first {cnt} of {n} projections; reconstruct_optimized "
+                           f"defaults (lanes 16, chunk 262, clip+pad); kernel "
+                           f"{st['kernel_seconds']:.2f} s (+{st.get('precompute_seconds', 0):.2f} s "
+                           f"precompute, excluded); full-basis updates")}
+        except Exception as e:  # the baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "unit": "GUp/s", "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

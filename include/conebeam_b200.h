@@ -1,0 +1,168 @@
+/*
+ * conebeam_b200.h -- C ABI of the B200-native FDK back-projection library
+ * (libconebeam_b200.so, built from paper_1401_3615_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's hot path: voxel-driven
+ * back-projection of filtered cone-beam projections into a float32 volume
+ * (reference: proj/src/kernel_ref.cpp:5-38, proj/src/kernel_opt.cpp:658-716,
+ * exposed there through proj/include/conebeam/capi.h:104-107).
+ *
+ * Conventions kept from the reference C API (proj/include/conebeam/capi.h):
+ *  - every function returns a cbb_status whose numeric values are identical
+ *    to cb_status (capi.h:20-29); the message of the last failure on the
+ *    calling thread is available from cbb_last_error() (capi.cpp:26-28);
+ *  - objects live behind opaque handles released with the matching *_free;
+ *  - stats out-parameters are nullable.
+ *
+ * Data layouts are the reference's (proj/include/conebeam/dataset.hpp:15-60,
+ * geometry.hpp:47-65): projections are row-major float32, index iy*W+ix;
+ * volumes are float32, index (z*L+y)*L+x; each projection matrix is 12
+ * doubles, column-major 3x4 (u = wx*a0 + wy*a3 + wz*a6 + a9, ...), cast to
+ * float inside the kernel exactly as the reference does (kernel_ref.cpp:11-13).
+ *
+ * Semantics: reconstructions ACCUMULATE into the given volume (vol +=), in
+ * projection order, like reconstruct_reference. In exact mode (the default)
+ * the result is bitwise identical to reconstruct_reference; on any error the
+ * host volume is left unchanged (the reference leaves it partially updated).
+ *
+ * No torch types appear here; device entry points take plain device
+ * pointers and a cudaStream_t passed as void*.
+ */
+#ifndef CONEBEAM_B200_H
+#define CONEBEAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same values as cb_status (proj/include/conebeam/capi.h:20-29). */
+typedef enum cbb_status {
+    CBB_OK = 0,
+    CBB_ERR_INVALID = 1,   /* bad arguments or configuration */
+    CBB_ERR_IO = 2,        /* open/read/write failure */
+    CBB_ERR_FORMAT = 3,    /* bad magic, version, or trailing bytes */
+    CBB_ERR_TRUNCATED = 4, /* payload shorter than the header promises */
+    CBB_ERR_GEOMETRY = 5,  /* degenerate geometry: a voxel with w == 0 */
+    CBB_ERR_NOMEM = 6,     /* host or device allocation failed */
+    CBB_ERR_INTERNAL = 7   /* CUDA / NCCL failure, no device, ... */
+} cbb_status;
+
+/* Replaces cb_status_name / cb_last_error (capi.h:31-32, capi.cpp:93-108). */
+const char* cbb_status_name(cbb_status status);
+const char* cbb_last_error(void);
+
+/* Library/device introspection. */
+const char* cbb_version(void);
+int32_t cbb_device_count(void);
+
+/* Volume descriptor (VolumeGeometry, proj/include/conebeam/geometry.hpp:15-34). */
+typedef struct cbb_volume_geometry {
+    int32_t edge_voxels; /* L */
+    double voxel_mm;
+    double origin_mm;    /* world coordinate of voxel index 0 */
+} cbb_volume_geometry;
+
+/* Kernel arithmetic variants. */
+enum {
+    CBB_MODE_EXACT = 0, /* bitwise equal to reconstruct_reference (default) */
+    CBB_MODE_FAST = 1   /* weight 1/w^2 as r*r with one reciprocal; relL2 ~1e-7 */
+};
+
+/* Options (the B200 counterpart of cb_opt_options, capi.h:84-91). */
+typedef struct cbb_options {
+    int32_t num_gpus;          /* 0 = all visible devices (whole-stack calls) */
+    const int32_t* device_ids; /* nullable: devices 0..num_gpus-1 */
+    int32_t batch;             /* projections per kernel launch, 1..64 (default 32) */
+    int32_t mode;              /* CBB_MODE_EXACT / CBB_MODE_FAST */
+    int32_t cull;              /* skip voxel tiles whose footprint misses the detector */
+    int32_t volume_is_zero;    /* caller promises the input volume is all +0: skip its upload */
+    int32_t slab_begin;        /* z-planes [slab_begin, slab_end) of the volume to update; */
+    int32_t slab_end;          /* 0, 0 = all planes (one process per GPU drives one slab) */
+} cbb_options;
+
+void cbb_options_defaults(cbb_options* options);
+
+/* Per-call statistics (cb_run_stats, capi.h:93-102, extended per phase). */
+typedef struct cbb_run_stats {
+    double total_seconds;      /* wall time of the call */
+    double h2d_seconds;        /* max over GPUs, device-timed */
+    double kernel_seconds;     /* max over GPUs, device-timed (pack + back-projection) */
+    double d2h_seconds;        /* max over GPUs, device-timed */
+    uint64_t voxel_updates;    /* full basis: L^3 * projections */
+    uint64_t guarded_batches;  /* batches that needed the guarded kernel */
+    int32_t num_gpus;
+    double per_gpu_kernel_seconds[8];
+} cbb_run_stats;
+
+/* ---- host-pointer entry points (the drop-in) ------------------------------ */
+
+/* One projection into the whole volume: backproject_reference
+ * (proj/src/kernel_ref.cpp:5-30, kernel_ref.hpp:77). Synchronous. The volume
+ * is uploaded, updated and downloaded on every call; prefer cbb_reconstruct
+ * or a session for stacks. */
+cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry,
+                           const float* img, int32_t width, int32_t height,
+                           const double* matrix12);
+
+/* All projections in order: reconstruct_reference / cb_reconstruct_optimized
+ * (proj/src/kernel_ref.cpp:32-38, capi.h:104-107). imgs holds count*height*width
+ * floats, mats count*12 doubles. Multi-GPU: z-slabs, one host thread per GPU. */
+cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry,
+                           const float* imgs, int32_t width, int32_t height,
+                           int32_t count, const double* mats,
+                           const cbb_options* options /* nullable */,
+                           cbb_run_stats* stats /* nullable */);
+
+/* ---- streaming session (RabbitCT-style per-projection module) ------------ */
+
+typedef struct cbb_session_s cbb_session;
+
+/* initial_volume (L^3 floats, nullable = zeros) is copied at creation. */
+cbb_status cbb_session_create(const cbb_volume_geometry* geometry, int32_t width,
+                              int32_t height, const float* initial_volume,
+                              const cbb_options* options, cbb_session** out);
+/* Enqueues one projection (copied before return); launches when a batch fills. */
+cbb_status cbb_session_backproject(cbb_session* s, const float* img, const double* matrix12);
+/* Flushes and writes the accumulated volume (L^3 floats) to vol_out. The
+ * session stays usable and keeps accumulating afterwards. */
+cbb_status cbb_session_finish(cbb_session* s, float* vol_out, cbb_run_stats* stats);
+void cbb_session_free(cbb_session* s);
+
+/* ---- device-resident entry points (plain device pointers) ---------------- */
+
+/* Layout of the packed projection buffer the back-projection kernel gathers
+ * from: per projection, quad_rows x quad_pitch float4 cells; cell (px,py)
+ * holds the four bilinear taps of detector position (px,py) with zeros
+ * outside the detector (zero-pad semantics of bilinear_sample_guarded). */
+cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* quad_pitch,
+                             int32_t* quad_rows, int64_t* bytes_per_projection);
+
+/* raw: count x height x width floats (device). packed: count packed
+ * projections (device, cbb_packed_layout bytes each). Enqueued on stream. */
+cbb_status cbb_pack_device(const float* raw, int32_t width, int32_t height, int32_t count,
+                           void* packed, void* stream);
+
+/* Back-projects count packed projections into a z-slab [z_begin, z_end) of
+ * the volume held on the device at vol_slab (voxel (0,0,z_begin) first,
+ * z-major). mats: count*12 doubles on the HOST (they travel as kernel
+ * parameters, i.e. constant memory). err_flag: device int (nullable) set to 1
+ * when a voxel hits w == 0; the caller must check it (cbb_reconstruct does).
+ * Enqueued on stream; returns after launch. */
+cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                  int32_t z_begin, int32_t z_end, const void* packed,
+                                  int32_t width, int32_t height, int32_t count,
+                                  const double* mats, const cbb_options* options,
+                                  int32_t* err_flag, void* stream);
+
+/* Number of kernel launches the last cbb_backproject_device / cbb_pack_device
+ * calls on this thread issued (for the bench's gpu_launches count). */
+uint64_t cbb_launch_count(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* CONEBEAM_B200_H */

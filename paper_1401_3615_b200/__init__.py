@@ -1,0 +1,23 @@
+"""paper_1401_3615_b200 -- B200-native voxel-driven FDK back-projection.
+
+Drop-in for the reference's hot path (proj/src/kernel_ref.cpp:5-38,
+proj/src/kernel_opt.cpp:658-716) through the C ABI in include/conebeam_b200.h.
+"""
+from .backproject import (MODE_EXACT, MODE_FAST, Options, Session, backproject,
+                          backproject_device, device_count, launch_count, pack_device,
+                          packed_layout, reconstruct, reconstruct_arrays)
+from .dataset import ProjectionStack, Volume, read_stack, read_volume, write_stack, write_volume
+from .errors import (ConebeamError, FormatError, GeometryError, InternalError, IOError_,
+                     OutOfMemoryError, TruncatedError, ValidationError)
+from .geometry import (TrajectoryConfig, VolumeGeometry, dehomogenize, forward_project,
+                       make_circular_trajectory, world_from_voxel)
+
+__all__ = [
+    "MODE_EXACT", "MODE_FAST", "Options", "Session", "backproject", "backproject_device",
+    "device_count", "launch_count", "pack_device", "packed_layout", "reconstruct",
+    "reconstruct_arrays", "ProjectionStack", "Volume", "read_stack", "read_volume",
+    "write_stack", "write_volume", "ConebeamError", "FormatError", "GeometryError",
+    "InternalError", "IOError_", "OutOfMemoryError", "TruncatedError", "ValidationError",
+    "TrajectoryConfig", "VolumeGeometry", "dehomogenize", "forward_project",
+    "make_circular_trajectory", "world_from_voxel",
+]

@@ -1,0 +1,120 @@
+"""ctypes binding of libconebeam_b200.so (declared in include/conebeam_b200.h).
+
+The product path has no fallback: if the library is missing or cannot be
+loaded, ``lib()`` raises. Nothing here imports the oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import InternalError, error_for_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libconebeam_b200.so")
+
+# Every symbol declared in include/conebeam_b200.h (checked by tests).
+EXPORTS = (
+    "cbb_status_name", "cbb_last_error", "cbb_version", "cbb_device_count",
+    "cbb_options_defaults", "cbb_backproject", "cbb_reconstruct",
+    "cbb_session_create", "cbb_session_backproject", "cbb_session_finish",
+    "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
+    "cbb_backproject_device", "cbb_launch_count",
+)
+
+
+class VolumeGeometryC(C.Structure):
+    _fields_ = [("edge_voxels", C.c_int32), ("voxel_mm", C.c_double),
+                ("origin_mm", C.c_double)]
+
+
+class OptionsC(C.Structure):
+    _fields_ = [("num_gpus", C.c_int32), ("device_ids", C.POINTER(C.c_int32)),
+                ("batch", C.c_int32), ("mode", C.c_int32), ("cull", C.c_int32),
+                ("volume_is_zero", C.c_int32), ("slab_begin", C.c_int32),
+                ("slab_end", C.c_int32)]
+
+
+class RunStatsC(C.Structure):
+    _fields_ = [("total_seconds", C.c_double), ("h2d_seconds", C.c_double),
+                ("kernel_seconds", C.c_double), ("d2h_seconds", C.c_double),
+                ("voxel_updates", C.c_uint64), ("guarded_batches", C.c_uint64),
+                ("num_gpus", C.c_int32), ("per_gpu_kernel_seconds", C.c_double * 8)]
+
+    def to_dict(self) -> dict:
+        return {
+            "total_seconds": self.total_seconds, "h2d_seconds": self.h2d_seconds,
+            "kernel_seconds": self.kernel_seconds, "d2h_seconds": self.d2h_seconds,
+            "voxel_updates": int(self.voxel_updates),
+            "guarded_batches": int(self.guarded_batches), "num_gpus": int(self.num_gpus),
+            "per_gpu_kernel_seconds": list(self.per_gpu_kernel_seconds)[: max(self.num_gpus, 0)],
+        }
+
+
+_lock = threading.Lock()
+_lib = None
+
+_FP = C.POINTER(C.c_float)
+_DP = C.POINTER(C.c_double)
+_VP = C.c_void_p
+
+
+def _declare(L) -> None:
+    L.cbb_status_name.restype = C.c_char_p
+    L.cbb_status_name.argtypes = [C.c_int]
+    L.cbb_last_error.restype = C.c_char_p
+    L.cbb_last_error.argtypes = []
+    L.cbb_version.restype = C.c_char_p
+    L.cbb_device_count.restype = C.c_int32
+    L.cbb_options_defaults.restype = None
+    L.cbb_options_defaults.argtypes = [C.POINTER(OptionsC)]
+    L.cbb_backproject.restype = C.c_int
+    L.cbb_backproject.argtypes = [_VP, C.POINTER(VolumeGeometryC), _VP, C.c_int32, C.c_int32, _VP]
+    L.cbb_reconstruct.restype = C.c_int
+    L.cbb_reconstruct.argtypes = [_VP, C.POINTER(VolumeGeometryC), _VP, C.c_int32, C.c_int32,
+                                  C.c_int32, _VP, C.POINTER(OptionsC), C.POINTER(RunStatsC)]
+    L.cbb_session_create.restype = C.c_int
+    L.cbb_session_create.argtypes = [C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32, _VP,
+                                     C.POINTER(OptionsC), C.POINTER(_VP)]
+    L.cbb_session_backproject.restype = C.c_int
+    L.cbb_session_backproject.argtypes = [_VP, _VP, _VP]
+    L.cbb_session_finish.restype = C.c_int
+    L.cbb_session_finish.argtypes = [_VP, _VP, C.POINTER(RunStatsC)]
+    L.cbb_session_free.restype = None
+    L.cbb_session_free.argtypes = [_VP]
+    L.cbb_packed_layout.restype = C.c_int
+    L.cbb_packed_layout.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+    L.cbb_pack_device.restype = C.c_int
+    L.cbb_pack_device.argtypes = [_VP, C.c_int32, C.c_int32, C.c_int32, _VP, _VP]
+    L.cbb_backproject_device.restype = C.c_int
+    L.cbb_backproject_device.argtypes = [_VP, C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32,
+                                         _VP, C.c_int32, C.c_int32, C.c_int32, _VP,
+                                         C.POINTER(OptionsC), _VP, _VP]
+    L.cbb_launch_count.restype = C.c_uint64
+    L.cbb_launch_count.argtypes = []
+
+
+def lib():
+    """Loads libconebeam_b200.so once; raises InternalError when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise InternalError(
+                    f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                    "(make -C paper_1401_3615_b200/csrc); there is no CPU fallback")
+            L = C.CDLL(LIB_PATH)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    """Raises the exception matching a non-zero cbb_status with cbb_last_error()."""
+    if status != 0:
+        msg = lib().cbb_last_error().decode(errors="replace")
+        raise error_for_status(status, msg)

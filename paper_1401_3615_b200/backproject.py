@@ -1,0 +1,263 @@
+"""Host-side mirror of the reference's back-projection interface, running on
+the B200 through the C ABI of libconebeam_b200.so.
+
+Reference interface                                 -> here
+  backproject_reference(Volume&, img, matrix)         -> backproject(vol, img, matrix)
+    (proj/include/conebeam/kernel_ref.hpp:77, proj/src/kernel_ref.cpp:5-30)
+  reconstruct_reference(Volume&, stack)               -> reconstruct(vol, stack)
+    (proj/src/kernel_ref.cpp:32-38)
+  reconstruct_optimized(vol, stack, OptOptions, stats)-> reconstruct(vol, stack, options, ...)
+    (proj/src/kernel_opt.cpp:658-716)
+Same argument meaning and error behaviour: geometry mismatch and w == 0 raise
+GeometryError, bad inputs raise ValidationError, the volume accumulates (+=).
+In exact mode the result is bitwise that of reconstruct_reference.
+
+There is no CPU path: every call goes through the CUDA library and raises if
+it cannot be loaded or no device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .dataset import ProjectionStack, Volume, check_same_geometry
+from .errors import ValidationError
+from .geometry import VolumeGeometry, validate_matrices
+
+MODE_EXACT = 0
+MODE_FAST = 1
+
+
+@dataclass
+class Options:
+    """cbb_options (include/conebeam_b200.h); B200 counterpart of OptOptions
+    (proj/include/conebeam/kernel_opt.hpp:121-133)."""
+
+    num_gpus: int = 0                 # 0 = all visible devices
+    device_ids: Optional[Sequence[int]] = None
+    batch: int = 32                   # projections per launch (1..64)
+    mode: int = MODE_EXACT
+    cull: bool = True
+    volume_is_zero: bool = False
+    slab: Optional[Sequence[int]] = None  # (z_begin, z_end) planes to update; None = all
+
+    def to_c(self):
+        o = _lib.OptionsC()
+        _lib.lib().cbb_options_defaults(C.byref(o))
+        o.num_gpus = int(self.num_gpus)
+        keep = None
+        if self.device_ids is not None:
+            keep = (C.c_int32 * len(self.device_ids))(*[int(d) for d in self.device_ids])
+            o.device_ids = C.cast(keep, C.POINTER(C.c_int32))
+            if self.num_gpus == 0:
+                o.num_gpus = len(self.device_ids)
+        o.batch = int(self.batch)
+        o.mode = int(self.mode)
+        o.cull = int(bool(self.cull))
+        o.volume_is_zero = int(bool(self.volume_is_zero))
+        if self.slab is not None:
+            o.slab_begin, o.slab_end = int(self.slab[0]), int(self.slab[1])
+        return o, keep
+
+
+def geometry_c(g: VolumeGeometry) -> _lib.VolumeGeometryC:
+    return _lib.VolumeGeometryC(int(g.edge_voxels), float(g.voxel_mm), float(g.origin_mm))
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _image(img, width=None, height=None) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    if a.ndim != 2:
+        raise ValidationError("ProjectionImage: expected a 2-D (height, width) array")
+    return a
+
+
+def backproject(vol: Volume, img, matrix, validate: bool = True) -> None:
+    """Accumulates one projection into the volume, in place.
+
+    Semantics of backproject_reference (proj/src/kernel_ref.cpp:5-30): the
+    image and volume are validated (finite values), the matrix is cast to
+    float, and a voxel with w == 0 raises GeometryError (on error the volume
+    is left unchanged here; the reference leaves it partially updated).
+    """
+    im = _image(img)
+    m = validate_matrices(matrix)
+    if m.shape[0] != 1:
+        raise ValidationError("backproject: expected one 3x4 matrix")
+    if validate:
+        if not np.isfinite(im).all():
+            raise ValidationError("ProjectionImage contains non-finite values")
+        vol.validate()
+    g = geometry_c(vol.geometry)
+    L = _lib.lib()
+    _lib.check(L.cbb_backproject(_ptr(vol.voxels), C.byref(g), _ptr(im), im.shape[1],
+                                 im.shape[0], _ptr(m)))
+
+
+def reconstruct(vol: Volume, stack: ProjectionStack, options: Optional[Options] = None,
+                validate: bool = True) -> dict:
+    """Back-projects every projection of the stack, in order, into vol (+=).
+
+    reconstruct_reference / cb_reconstruct_optimized semantics; returns the
+    per-phase run statistics (cb_run_stats counterpart). Multi-GPU via
+    options.num_gpus: z-slabs, one per device.
+    """
+    if validate:
+        stack.validate()
+        vol.validate()
+    check_same_geometry(vol, stack, "reconstruct")
+    opt = options or Options()
+    oc, _keep = opt.to_c()
+    g = geometry_c(vol.geometry)
+    st = _lib.RunStatsC()
+    L = _lib.lib()
+    _lib.check(L.cbb_reconstruct(_ptr(vol.voxels), C.byref(g), _ptr(stack.images),
+                                 stack.width, stack.height, stack.count,
+                                 _ptr(stack.matrices), C.byref(oc), C.byref(st)))
+    return st.to_dict()
+
+
+def reconstruct_arrays(voxels: np.ndarray, geometry: VolumeGeometry, images: np.ndarray,
+                       matrices: np.ndarray, options: Optional[Options] = None) -> dict:
+    """Array-level reconstruct without validation scans (bench e2e leg):
+    voxels (L,L,L) float32 accumulated in place; images (N,H,W) float32 (pinned
+    or pageable host memory); matrices (N,12) float64."""
+    if voxels.dtype != np.float32 or not voxels.flags.c_contiguous:
+        raise ValidationError("voxels must be C-contiguous float32")
+    if images.dtype != np.float32 or not images.flags.c_contiguous or images.ndim != 3:
+        raise ValidationError("images must be C-contiguous float32 (N, H, W)")
+    m = validate_matrices(matrices)
+    opt = options or Options()
+    oc, _keep = opt.to_c()
+    g = geometry_c(geometry)
+    st = _lib.RunStatsC()
+    _lib.check(_lib.lib().cbb_reconstruct(voxels.ctypes.data, C.byref(g), images.ctypes.data,
+                                          images.shape[2], images.shape[1], images.shape[0],
+                                          _ptr(m), C.byref(oc), C.byref(st)))
+    return st.to_dict()
+
+
+class Session:
+    """Streaming per-projection back-projection (cbb_session_*), the
+    RabbitCT-style module interface: feed projections one by one, read the
+    volume with finish()."""
+
+    def __init__(self, geometry: VolumeGeometry, width: int, height: int,
+                 initial_volume: Optional[np.ndarray] = None,
+                 options: Optional[Options] = None):
+        geometry.validate()
+        self.geometry = geometry
+        self.width = int(width)
+        self.height = int(height)
+        self._init = None
+        if initial_volume is not None:
+            self._init = np.ascontiguousarray(initial_volume, dtype=np.float32)
+            if self._init.size != geometry.voxel_count:
+                raise ValidationError("Session: initial volume must hold L^3 voxels")
+        oc, self._keep = (options or Options()).to_c()
+        g = geometry_c(geometry)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().cbb_session_create(
+            C.byref(g), self.width, self.height,
+            None if self._init is None else _ptr(self._init), C.byref(oc), C.byref(h)))
+        self._h = h
+
+    def backproject(self, img, matrix) -> None:
+        im = _image(img)
+        if im.shape != (self.height, self.width):
+            raise ValidationError("Session: image dimensions differ from the session's")
+        m = validate_matrices(matrix)
+        _lib.check(_lib.lib().cbb_session_backproject(self._h, _ptr(im), _ptr(m)))
+
+    def finish(self) -> tuple:
+        L = self.geometry.edge_voxels
+        out = np.empty((L, L, L), dtype=np.float32)
+        st = _lib.RunStatsC()
+        _lib.check(_lib.lib().cbb_session_finish(self._h, _ptr(out), C.byref(st)))
+        return out, st.to_dict()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.lib().cbb_session_free(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --- device-resident path (torch tensors as plain device memory) ---------------
+
+def packed_layout(width: int, height: int) -> tuple:
+    """(quad_pitch, quad_rows, bytes_per_projection) of the packed gather layout."""
+    qp, qr, nb = C.c_int32(), C.c_int32(), C.c_int64()
+    _lib.check(_lib.lib().cbb_packed_layout(int(width), int(height), C.byref(qp), C.byref(qr),
+                                            C.byref(nb)))
+    return qp.value, qr.value, nb.value
+
+
+def pack_device(raw, packed, stream=None) -> None:
+    """raw: CUDA float32 tensor (N, H, W); packed: CUDA tensor with at least
+    N * bytes_per_projection bytes. Enqueued on `stream` (torch stream or None
+    for the current stream)."""
+    import torch
+
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
+        raise ValidationError("pack_device: raw must be a contiguous CUDA float32 (N, H, W) tensor")
+    n, h, w = raw.shape
+    _, _, nb = packed_layout(w, h)
+    if packed.numel() * packed.element_size() < n * nb:
+        raise ValidationError("pack_device: packed buffer too small")
+    s = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    _lib.check(_lib.lib().cbb_pack_device(raw.data_ptr(), w, h, n, packed.data_ptr(),
+                                          C.c_void_p(s.cuda_stream)))
+
+
+def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: int, packed,
+                       width: int, height: int, count: int, matrices: np.ndarray,
+                       options: Optional[Options] = None, err_flag=None, stream=None,
+                       first: int = 0) -> None:
+    """Enqueues the back-projection of `count` packed projections (starting at
+    packed projection `first`) into a device z-slab [z_begin, z_end)."""
+    import torch
+
+    if not (vol_slab.is_cuda and vol_slab.dtype == torch.float32 and vol_slab.is_contiguous()):
+        raise ValidationError("backproject_device: vol_slab must be a contiguous CUDA float32 tensor")
+    L = geometry.edge_voxels
+    if vol_slab.numel() < (z_end - z_begin) * L * L:
+        raise ValidationError("backproject_device: slab tensor too small")
+    m = validate_matrices(matrices)
+    if m.shape[0] < count:
+        raise ValidationError("backproject_device: fewer matrices than projections")
+    _, _, nb = packed_layout(width, height)
+    oc, _keep = (options or Options()).to_c()
+    g = geometry_c(geometry)
+    s = stream if stream is not None else torch.cuda.current_stream(vol_slab.device)
+    _lib.check(_lib.lib().cbb_backproject_device(
+        vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end),
+        packed.data_ptr() + int(first) * nb, int(width), int(height), int(count), _ptr(m),
+        C.byref(oc), None if err_flag is None else err_flag.data_ptr(),
+        C.c_void_p(s.cuda_stream)))
+
+
+def launch_count() -> int:
+    return int(_lib.lib().cbb_launch_count())
+
+
+def device_count() -> int:
+    return int(_lib.lib().cbb_device_count())

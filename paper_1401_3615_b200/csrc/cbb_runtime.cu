@@ -1,0 +1,708 @@
+// cbb_runtime.cu -- host runtime and C ABI of libconebeam_b200.so.
+//
+// Implements include/conebeam_b200.h: error model mirroring the reference C
+// API (proj/src/capi.cpp:26-68), the guard decision per batch, launches of the
+// sm_100a kernels in bp_kernels.cuh, and the staging pipeline:
+//   host projections --(pinned, double-buffered cudaMemcpyAsync on a copy
+//   stream)--> raw ring slot --(pack_quads on the compute stream)--> packed
+//   ring slot --(bp_kernel, matrices as kernel parameters = constant bank)-->
+//   register partial sums --> volume slab in HBM.
+// Multi-GPU (one process): the volume is split into z-slabs, one per device;
+// every device receives every projection batch; slabs are downloaded into the
+// caller's volume at the end (no reduction: voxel ownership is disjoint).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/conebeam_b200.h"
+#include "bp_kernels.cuh"
+
+namespace cbb {
+
+// ---------------------------------------------------------------------------
+// Errors (reference: proj/include/conebeam/errors.hpp:10-44, capi.cpp:30-60)
+// ---------------------------------------------------------------------------
+
+struct Error : std::runtime_error {
+    cbb_status status;
+    Error(cbb_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+thread_local std::string g_last_error;
+thread_local uint64_t g_launches = 0;
+
+[[noreturn]] void fail(cbb_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Error(s, buf);
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess)
+        return;
+    cudaGetLastError(); // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation)
+        fail(CBB_ERR_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+    fail(CBB_ERR_INTERNAL, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call) check_cuda((call), #call)
+
+template <typename Fn>
+cbb_status guarded(Fn&& fn) noexcept {
+    try {
+        fn();
+        return CBB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of memory";
+        return CBB_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return CBB_ERR_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return CBB_ERR_INTERNAL;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Validation (VolumeGeometry::validate, proj/src/geometry.cpp:17-24;
+// ProjectionMatrix::validate :35-39)
+// ---------------------------------------------------------------------------
+
+void validate_geometry(const cbb_volume_geometry* g) {
+    if (!g)
+        fail(CBB_ERR_INVALID, "null volume geometry");
+    if (g->edge_voxels < 1)
+        fail(CBB_ERR_INVALID, "VolumeGeometry: field 'edge_voxels' must be >= 1");
+    if (!(g->voxel_mm > 0.0) || !std::isfinite(g->voxel_mm))
+        fail(CBB_ERR_INVALID, "VolumeGeometry: field 'voxel_mm' must be positive and finite");
+    if (!std::isfinite(g->origin_mm))
+        fail(CBB_ERR_INVALID, "VolumeGeometry: field 'origin_mm' must be finite");
+    if (g->edge_voxels > 4096)
+        fail(CBB_ERR_INVALID, "VolumeGeometry: edge_voxels > 4096 not supported");
+}
+
+void validate_detector(int32_t w, int32_t h) {
+    if (w < 1 || h < 1)
+        fail(CBB_ERR_INVALID, "ProjectionImage: dimensions must be >= 1");
+    // packed cell indices are formed exactly in float: must stay below 2^23
+    const double cells = (double)quad_pitch_cells(w) * quad_rows(h);
+    if (cells >= 8388608.0 - 16)
+        fail(CBB_ERR_INVALID, "detector %dx%d too large for the packed layout", w, h);
+}
+
+void validate_matrices(const double* mats, int32_t count) {
+    for (int32_t p = 0; p < count; ++p)
+        for (int i = 0; i < 12; ++i)
+            if (!std::isfinite(mats[12 * (size_t)p + i]))
+                fail(CBB_ERR_INVALID, "ProjectionMatrix: field 'a[%d]' must be finite", i);
+}
+
+cbb_options resolve_options(const cbb_options* o) {
+    cbb_options r;
+    cbb_options_defaults(&r);
+    if (o)
+        r = *o;
+    if (r.batch < 1 || r.batch > kMaxBatch)
+        fail(CBB_ERR_INVALID, "options: batch must be in [1, %d]", kMaxBatch);
+    if (r.mode != CBB_MODE_EXACT && r.mode != CBB_MODE_FAST)
+        fail(CBB_ERR_INVALID, "options: unknown mode %d", r.mode);
+    if (r.num_gpus < 0)
+        fail(CBB_ERR_INVALID, "options: num_gpus must be >= 0");
+    if (r.slab_begin < 0 || r.slab_end < 0 || (r.slab_end != 0 && r.slab_end <= r.slab_begin))
+        fail(CBB_ERR_INVALID, "options: bad slab [%d, %d)", r.slab_begin, r.slab_end);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Guard decision. A batch may run the unguarded kernel when, for every
+// projection, w > 0 with margin at the 8 corners of the slab box and the
+// projected corners satisfy |ix|,|iy| < 1e8. w is affine in the voxel
+// coordinates, so positive corners imply w > 0 inside; u/w and v/w are
+// linear-fractional with a positive denominator, hence monotone along every
+// line and extremal at box vertices. The float kernel differs from the double
+// evaluation by a few ulps, far inside both margins. Matrices containing a
+// -0.0 coefficient are sent to the guarded kernel too (signed-zero corner
+// cases of the IEEE division are then handled by the reference arithmetic).
+// ---------------------------------------------------------------------------
+
+bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_begin, int z_end) {
+    const float fa0 = 0.0f;
+    for (int i = 0; i < 12; ++i) {
+        const float f = (float)a[i];
+        if (f == fa0 && std::signbit(f))
+            return false;
+    }
+    const int L = g.edge_voxels;
+    const double lo = g.origin_mm;
+    const double hi = g.origin_mm + (L - 1) * g.voxel_mm;
+    const double zlo = g.origin_mm + z_begin * g.voxel_mm;
+    const double zhi = g.origin_mm + (z_end - 1) * g.voxel_mm;
+    for (int c = 0; c < 8; ++c) {
+        const double wx = (c & 1) ? hi : lo;
+        const double wy = (c & 2) ? hi : lo;
+        const double wz = (c & 4) ? zhi : zlo;
+        const double u = wx * a[0] + wy * a[3] + wz * a[6] + a[9];
+        const double v = wx * a[1] + wy * a[4] + wz * a[7] + a[10];
+        const double w = wx * a[2] + wy * a[5] + wz * a[8] + a[11];
+        const double scale = std::fabs(wx * a[2]) + std::fabs(wy * a[5]) +
+                             std::fabs(wz * a[8]) + std::fabs(a[11]);
+        if (!(w > 1e-4 * scale) || !(w > 1e-30))
+            return false;
+        if (!(std::fabs(u / w) < 1e8) || !(std::fabs(v / w) < 1e8))
+            return false;
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+
+constexpr int kR = 8; // voxels per thread along z
+
+void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaStream_t st) {
+    const int qp = quad_pitch_cells(W);
+    const int qr = quad_rows(H);
+    dim3 grid((qp + 127) / 128, qr, count);
+    pack_quads<<<grid, 128, 0, st>>>(raw, W, H, static_cast<float4*>(packed), qp, qr);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+template <int MODE, bool GUARD>
+void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
+    dim3 block(kBlockX, kBlockY);
+    dim3 grid((args.L + kBlockX - 1) / kBlockX, (args.L + kBlockY - 1) / kBlockY,
+              (nz + kR - 1) / kR);
+    bp_kernel<kR, MODE, GUARD><<<grid, block, 0, st>>>(args, mats);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
+// Launches ceil(count/batch) back-projection kernels over a slab. Returns the
+// number of guarded launches.
+uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z_begin,
+                            int z_end, const void* packed, int W, int H, int count,
+                            const double* mats, const cbb_options& opt, int* err,
+                            cudaStream_t st) {
+    const int qp = quad_pitch_cells(W);
+    const int qr = quad_rows(H);
+    const long long proj_bytes = (long long)qp * qr * 16;
+    BpArgs args;
+    args.vol = vol_slab;
+    args.proj_bytes = proj_bytes;
+    args.L = g.edge_voxels;
+    args.z_begin = z_begin;
+    args.z_end = z_end;
+    args.O = (float)g.origin_mm;
+    args.MM = (float)g.voxel_mm;
+    args.Wf = (float)W;
+    args.Hf = (float)H;
+    args.qpitchf = (float)qp;
+    args.cell_bias = (float)(2 * qp + 2) + 8388608.0f;
+    args.err = err;
+    uint64_t guarded_launches = 0;
+    const int nz = z_end - z_begin;
+    if (nz <= 0 || count <= 0)
+        return 0;
+    for (int first = 0; first < count; first += opt.batch) {
+        const int n = std::min(opt.batch, count - first);
+        BpMats m;
+        bool safe = true;
+        for (int p = 0; p < n; ++p) {
+            const double* a = mats + 12 * (size_t)(first + p);
+            for (int i = 0; i < 12; ++i)
+                m.a[p][i] = (float)a[i];
+            safe = safe && projection_is_safe(a, g, z_begin, z_end);
+        }
+        if (!safe && !err)
+            fail(CBB_ERR_INVALID,
+                 "guarded batch requires an error flag (matrix near w == 0 over the volume)");
+        args.count = n;
+        args.packed = static_cast<const char*>(packed) + (long long)first * proj_bytes -
+                      (long long)kMagic * 16;
+        if (opt.mode == CBB_MODE_EXACT) {
+            if (safe)
+                launch_bp_t<0, false>(args, m, nz, st);
+            else
+                launch_bp_t<0, true>(args, m, nz, st);
+        } else {
+            if (safe)
+                launch_bp_t<1, false>(args, m, nz, st);
+            else
+                launch_bp_t<1, true>(args, m, nz, st);
+        }
+        guarded_launches += safe ? 0 : 1;
+    }
+    return guarded_launches;
+}
+
+// ---------------------------------------------------------------------------
+// Per-device worker: slab volume, raw/packed double buffers, streams, events.
+// ---------------------------------------------------------------------------
+
+struct Worker {
+    int device = 0;
+    int z_begin = 0, z_end = 0;
+    float* d_vol = nullptr;
+    float* d_raw[2] = {nullptr, nullptr};
+    void* d_packed[2] = {nullptr, nullptr};
+    int* d_err = nullptr;
+    cudaStream_t copy = nullptr, compute = nullptr;
+    cudaEvent_t h2d_done[2] = {}, raw_free[2] = {};
+    cudaEvent_t k_beg = nullptr, k_end = nullptr, c_beg = nullptr, c_end = nullptr;
+    double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
+    uint64_t guarded = 0;
+    bool started = false;
+
+    ~Worker() {
+        if (!copy)
+            return;
+        cudaSetDevice(device);
+        cudaStreamSynchronize(copy);
+        cudaStreamSynchronize(compute);
+        cudaFree(d_vol);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(d_raw[i]);
+            cudaFree(d_packed[i]);
+            cudaEventDestroy(h2d_done[i]);
+            cudaEventDestroy(raw_free[i]);
+        }
+        cudaFree(d_err);
+        cudaEventDestroy(k_beg);
+        cudaEventDestroy(k_end);
+        cudaEventDestroy(c_beg);
+        cudaEventDestroy(c_end);
+        cudaStreamDestroy(copy);
+        cudaStreamDestroy(compute);
+    }
+};
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+}
+
+struct Pipeline {
+    cbb_volume_geometry g{};
+    int W = 0, H = 0;
+    cbb_options opt{};
+    std::vector<std::unique_ptr<Worker>> workers;
+    float* h_stage[2] = {nullptr, nullptr}; // pinned staging (batch x H x W)
+    int stage_fill = 0;                     // projections staged in the current slot
+    int slot = 0;                           // current staging / ring slot
+    std::vector<double> stage_mats;         // matrices of the staged batch
+    uint64_t submitted = 0;
+    size_t raw_bytes_per_proj = 0;
+    size_t packed_bytes_per_proj = 0;
+
+    ~Pipeline() {
+        workers.clear();
+        for (int i = 0; i < 2; ++i)
+            if (h_stage[i])
+                cudaFreeHost(h_stage[i]);
+    }
+
+    void init(const cbb_volume_geometry& geom, int width, int height, const cbb_options& o,
+              const float* initial_volume) {
+        g = geom;
+        W = width;
+        H = height;
+        opt = o;
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (ndev < 1)
+            fail(CBB_ERR_INTERNAL, "no CUDA device available");
+        if (opt.slab_end > g.edge_voxels)
+            fail(CBB_ERR_INVALID, "options: slab_end %d beyond L = %d", opt.slab_end,
+                 g.edge_voxels);
+        const int s0 = opt.slab_end ? opt.slab_begin : 0;
+        const int s1 = opt.slab_end ? opt.slab_end : g.edge_voxels;
+        int ng = opt.num_gpus > 0 ? opt.num_gpus : ndev;
+        ng = std::min(ng, s1 - s0);
+        if (!opt.device_ids && ng > ndev)
+            fail(CBB_ERR_INVALID, "options: num_gpus %d exceeds %d visible devices", ng, ndev);
+        raw_bytes_per_proj = (size_t)W * H * sizeof(float);
+        packed_bytes_per_proj = (size_t)quad_pitch_cells(W) * quad_rows(H) * 16;
+        const int L = g.edge_voxels;
+        const size_t plane = (size_t)L * L;
+        for (int i = 0; i < ng; ++i) {
+            auto w = std::make_unique<Worker>();
+            w->device = opt.device_ids ? opt.device_ids[i] : i;
+            if (w->device < 0 || w->device >= ndev)
+                fail(CBB_ERR_INVALID, "options: device id %d not visible", w->device);
+            w->z_begin = s0 + (int)((long long)(s1 - s0) * i / ng);
+            w->z_end = s0 + (int)((long long)(s1 - s0) * (i + 1) / ng);
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));
+            for (int s = 0; s < 2; ++s) {
+                CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
+                CK(cudaMalloc(&w->d_raw[s], raw_bytes_per_proj * opt.batch));
+                CK(cudaMalloc(&w->d_packed[s], packed_bytes_per_proj * opt.batch));
+            }
+            CK(cudaEventCreate(&w->k_beg));
+            CK(cudaEventCreate(&w->k_end));
+            CK(cudaEventCreate(&w->c_beg));
+            CK(cudaEventCreate(&w->c_end));
+            const size_t slab = plane * (w->z_end - w->z_begin);
+            CK(cudaMalloc(&w->d_vol, std::max<size_t>(slab, 1) * sizeof(float)));
+            CK(cudaMalloc(&w->d_err, sizeof(int)));
+            CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
+            CK(cudaEventRecord(w->c_beg, w->copy));
+            if (initial_volume && !opt.volume_is_zero)
+                CK(cudaMemcpyAsync(w->d_vol, initial_volume + plane * w->z_begin,
+                                   slab * sizeof(float), cudaMemcpyHostToDevice, w->copy));
+            else
+                CK(cudaMemsetAsync(w->d_vol, 0, slab * sizeof(float), w->copy));
+            CK(cudaEventRecord(w->c_end, w->copy));
+            CK(cudaStreamWaitEvent(w->compute, w->c_end, 0));
+            workers.push_back(std::move(w));
+        }
+        for (int s = 0; s < 2; ++s)
+            CK(cudaHostAlloc(&h_stage[s], raw_bytes_per_proj * opt.batch, cudaHostAllocPortable));
+        stage_mats.assign(12 * (size_t)opt.batch, 0.0);
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->h2d_s += elapsed_s(w->c_beg, w->c_end);
+        }
+    }
+
+    // Issues one batch of n projections from host memory src (pinned or not)
+    // to every worker. The caller guarantees src stays valid until the
+    // corresponding h2d_done events complete (wait_slot).
+    void issue(const float* src, const double* mats, int n) {
+        const size_t bytes = raw_bytes_per_proj * n;
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            // raw[slot] may still be read by the pack of batch (k-2)
+            CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
+            CK(cudaMemcpyAsync(w->d_raw[slot], src, bytes, cudaMemcpyHostToDevice, w->copy));
+            CK(cudaEventRecord(w->h2d_done[slot], w->copy));
+            CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
+            if (!w->started) {
+                CK(cudaEventRecord(w->k_beg, w->compute));
+                w->started = true;
+            }
+            launch_pack(w->d_raw[slot], W, H, n, w->d_packed[slot], w->compute);
+            CK(cudaEventRecord(w->raw_free[slot], w->compute));
+            w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end,
+                                             w->d_packed[slot], W, H, n, mats, opt,
+                                             w->d_err, w->compute);
+        }
+        submitted += n;
+        slot ^= 1;
+    }
+
+    // Blocks until no device still reads the staging slot s.
+    void wait_slot(int s) {
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->h2d_done[s]));
+        }
+    }
+
+    void stage_one(const float* img, const double* m) {
+        if (stage_fill == 0)
+            wait_slot(slot);
+        std::memcpy(h_stage[slot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
+        std::memcpy(stage_mats.data() + 12 * (size_t)stage_fill, m, 12 * sizeof(double));
+        if (++stage_fill == opt.batch)
+            flush();
+    }
+
+    void flush() {
+        if (stage_fill == 0)
+            return;
+        issue(h_stage[slot], stage_mats.data(), stage_fill);
+        stage_fill = 0;
+    }
+
+    // Whole-stack submission straight from the caller's buffer: pinned
+    // buffers are copied asynchronously in place, pageable ones are staged
+    // through the pinned double buffer.
+    void submit_stack(const float* imgs, const double* mats, int count) {
+        cudaPointerAttributes attr;
+        bool pinned = false;
+        if (cudaPointerGetAttributes(&attr, imgs) == cudaSuccess)
+            pinned = attr.type == cudaMemoryTypeHost;
+        else
+            cudaGetLastError();
+        for (int first = 0; first < count; first += opt.batch) {
+            const int n = std::min(opt.batch, count - first);
+            const float* src = imgs + (size_t)first * W * H;
+            if (pinned) {
+                issue(src, mats + 12 * (size_t)first, n);
+            } else {
+                wait_slot(slot);
+                std::memcpy(h_stage[slot], src, raw_bytes_per_proj * n);
+                issue(h_stage[slot], mats + 12 * (size_t)first, n);
+            }
+        }
+    }
+
+    // Waits for all work, checks the w == 0 flag, downloads slabs into vol_out.
+    void finish(float* vol_out) {
+        flush();
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (w->started) {
+                CK(cudaEventRecord(w->k_end, w->compute));
+            }
+        }
+        int err_any = 0;
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamSynchronize(w->compute));
+            if (w->started) {
+                w->kernel_s += elapsed_s(w->k_beg, w->k_end);
+                w->started = false;
+            }
+            int e = 0;
+            CK(cudaMemcpy(&e, w->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+            err_any |= e;
+        }
+        if (err_any)
+            fail(CBB_ERR_GEOMETRY, "backprojection hit a voxel with w == 0");
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            const size_t slab = plane * (w->z_end - w->z_begin);
+            CK(cudaEventRecord(w->c_beg, w->compute));
+            CK(cudaMemcpyAsync(vol_out + plane * w->z_begin, w->d_vol, slab * sizeof(float),
+                               cudaMemcpyDeviceToHost, w->compute));
+            CK(cudaEventRecord(w->c_end, w->compute));
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->d2h_s += elapsed_s(w->c_beg, w->c_end);
+        }
+    }
+
+    void fill_stats(cbb_run_stats* st, double total) const {
+        if (!st)
+            return;
+        std::memset(st, 0, sizeof *st);
+        st->total_seconds = total;
+        st->num_gpus = (int32_t)workers.size();
+        uint64_t planes = 0;
+        for (const auto& w : workers)
+            planes += (uint64_t)(w->z_end - w->z_begin);
+        st->voxel_updates = (uint64_t)g.edge_voxels * g.edge_voxels * planes * submitted;
+        for (size_t i = 0; i < workers.size(); ++i) {
+            const auto& w = *workers[i];
+            st->h2d_seconds = std::max(st->h2d_seconds, w.h2d_s);
+            st->kernel_seconds = std::max(st->kernel_seconds, w.kernel_s);
+            st->d2h_seconds = std::max(st->d2h_seconds, w.d2h_s);
+            st->guarded_batches += w.guarded;
+            if (i < 8)
+                st->per_gpu_kernel_seconds[i] = w.kernel_s;
+        }
+    }
+};
+
+} // namespace cbb
+
+using namespace cbb;
+
+struct cbb_session_s {
+    Pipeline pipe;
+    std::chrono::steady_clock::time_point t0;
+};
+
+extern "C" {
+
+const char* cbb_status_name(cbb_status status) {
+    switch (status) {
+    case CBB_OK: return "ok";
+    case CBB_ERR_INVALID: return "invalid argument";
+    case CBB_ERR_IO: return "i/o error";
+    case CBB_ERR_FORMAT: return "format error";
+    case CBB_ERR_TRUNCATED: return "truncated file";
+    case CBB_ERR_GEOMETRY: return "geometry error";
+    case CBB_ERR_NOMEM: return "out of memory";
+    case CBB_ERR_INTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+const char* cbb_last_error(void) { return g_last_error.c_str(); }
+
+const char* cbb_version(void) { return "conebeam_b200 0.1 (sm_100a)"; }
+
+int32_t cbb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t cbb_launch_count(void) { return g_launches; }
+
+void cbb_options_defaults(cbb_options* o) {
+    if (!o)
+        return;
+    o->num_gpus = 0;
+    o->device_ids = nullptr;
+    o->batch = 32;
+    o->mode = CBB_MODE_EXACT;
+    o->cull = 1;
+    o->volume_is_zero = 0;
+    o->slab_begin = 0;
+    o->slab_end = 0;
+}
+
+cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int32_t* qrows,
+                             int64_t* bytes) {
+    return guarded([&] {
+        validate_detector(width, height);
+        if (qpitch)
+            *qpitch = quad_pitch_cells(width);
+        if (qrows)
+            *qrows = quad_rows(height);
+        if (bytes)
+            *bytes = (int64_t)quad_pitch_cells(width) * quad_rows(height) * 16;
+    });
+}
+
+cbb_status cbb_pack_device(const float* raw, int32_t width, int32_t height, int32_t count,
+                           void* packed, void* stream) {
+    return guarded([&] {
+        if (!raw || !packed || count < 0)
+            fail(CBB_ERR_INVALID, "cbb_pack_device: null argument");
+        validate_detector(width, height);
+        if (count > 65535)
+            fail(CBB_ERR_INVALID, "cbb_pack_device: count > 65535 per call");
+        if (count == 0)
+            return;
+        launch_pack(raw, width, height, count, packed, static_cast<cudaStream_t>(stream));
+    });
+}
+
+cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                  int32_t z_begin, int32_t z_end, const void* packed,
+                                  int32_t width, int32_t height, int32_t count,
+                                  const double* mats, const cbb_options* options,
+                                  int32_t* err_flag, void* stream) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (!vol_slab || !packed || !mats)
+            fail(CBB_ERR_INVALID, "cbb_backproject_device: null argument");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin > z_end)
+            fail(CBB_ERR_INVALID, "cbb_backproject_device: bad slab [%d, %d)", z_begin, z_end);
+        validate_matrices(mats, count);
+        const cbb_options opt = resolve_options(options);
+        launch_backproject(vol_slab, *geometry, z_begin, z_end, packed, width, height, count,
+                           mats, opt, err_flag, static_cast<cudaStream_t>(stream));
+    });
+}
+
+cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, const float* imgs,
+                           int32_t width, int32_t height, int32_t count, const double* mats,
+                           const cbb_options* options, cbb_run_stats* stats) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!vol || !imgs || !mats)
+            fail(CBB_ERR_INVALID, "cbb_reconstruct: null argument");
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (count < 1)
+            fail(CBB_ERR_INVALID, "ProjectionStack: at least one projection required");
+        validate_matrices(mats, count);
+        const cbb_options opt = resolve_options(options);
+        Pipeline pipe;
+        pipe.init(*geometry, width, height, opt, vol);
+        pipe.submit_stack(imgs, mats, count);
+        // download into a private buffer first so a failure leaves vol intact
+        const size_t n = (size_t)geometry->edge_voxels * geometry->edge_voxels *
+                         geometry->edge_voxels;
+        if (opt.volume_is_zero) {
+            pipe.finish(vol);
+        } else {
+            std::vector<float> out(n);
+            pipe.finish(out.data());
+            const size_t plane = (size_t)geometry->edge_voxels * geometry->edge_voxels;
+            const int s0 = opt.slab_end ? opt.slab_begin : 0;
+            const int s1 = opt.slab_end ? opt.slab_end : geometry->edge_voxels;
+            std::memcpy(vol + plane * s0, out.data() + plane * s0,
+                        plane * (s1 - s0) * sizeof(float));
+        }
+        const double total =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        pipe.fill_stats(stats, total);
+    });
+}
+
+cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry, const float* img,
+                           int32_t width, int32_t height, const double* matrix12) {
+    cbb_options o;
+    cbb_options_defaults(&o);
+    o.num_gpus = 1;
+    o.batch = 1;
+    return cbb_reconstruct(vol, geometry, img, width, height, 1, matrix12, &o, nullptr);
+}
+
+cbb_status cbb_session_create(const cbb_volume_geometry* geometry, int32_t width,
+                              int32_t height, const float* initial_volume,
+                              const cbb_options* options, cbb_session** out) {
+    return guarded([&] {
+        if (!out)
+            fail(CBB_ERR_INVALID, "cbb_session_create: null argument");
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        const cbb_options opt = resolve_options(options);
+        auto s = std::make_unique<cbb_session_s>();
+        s->t0 = std::chrono::steady_clock::now();
+        s->pipe.init(*geometry, width, height, opt, initial_volume);
+        *out = s.release();
+    });
+}
+
+cbb_status cbb_session_backproject(cbb_session* s, const float* img, const double* m) {
+    return guarded([&] {
+        if (!s || !img || !m)
+            fail(CBB_ERR_INVALID, "cbb_session_backproject: null argument");
+        validate_matrices(m, 1);
+        s->pipe.stage_one(img, m);
+    });
+}
+
+cbb_status cbb_session_finish(cbb_session* s, float* vol_out, cbb_run_stats* stats) {
+    return guarded([&] {
+        if (!s || !vol_out)
+            fail(CBB_ERR_INVALID, "cbb_session_finish: null argument");
+        s->pipe.finish(vol_out);
+        const double total =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - s->t0).count();
+        s->pipe.fill_stats(stats, total);
+    });
+}
+
+void cbb_session_free(cbb_session* s) { delete s; }
+
+} // extern "C"

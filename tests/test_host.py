@@ -1,0 +1,192 @@
+"""CPU: host-side logic -- geometry conventions, file formats, generator
+determinism, the C-ABI library's exported surface (no compute calls)."""
+import ctypes
+import math
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_1401_3615_b200 as pkg
+from paper_1401_3615_b200 import synth
+from paper_1401_3615_b200.geometry import (TrajectoryConfig, VolumeGeometry, dehomogenize,
+                                           forward_project, make_circular_trajectory)
+
+
+def small_config(n=1, rng=2.0 * math.pi):
+    return TrajectoryConfig(n, 750.0, 1200.0, 1248, 960, 0.32, rng)
+
+
+# --- geometry (restates proj/tests/test_geometry.cpp:172-271) -----------------
+
+def test_trajectory_isocenter_normalised_and_centred():
+    for m in make_circular_trajectory(small_config(17)):
+        u, v, w = forward_project(m, 0.0, 0.0, 0.0)
+        assert abs(w - 1.0) <= 1e-9
+        ix, iy = dehomogenize(u, v, w)
+        assert abs(ix - 623.5) <= 1e-6 and abs(iy - 479.5) <= 1e-6
+
+
+def test_trajectory_matches_pinhole_oracle():
+    c = small_config(5, 3.0)
+    ms = make_circular_trajectory(c)
+    r = synth.SplitMix64(4242)
+    for i, m in enumerate(ms):
+        ang = c.angular_range_rad * i / c.num_projections
+        cs, sn = math.cos(ang), math.sin(ang)
+        R, f = c.source_isocenter_mm, c.source_detector_mm / c.pixel_size_mm
+        cu, cv = 0.5 * (c.detector_width - 1), 0.5 * (c.detector_height - 1)
+        rot = np.array([[-sn, cs, 0.0], [0.0, 0.0, 1.0], [-cs, -sn, 0.0]])
+        src = np.array([R * cs, R * sn, 0.0])
+        K = np.array([[f, 0, cu], [0, f, cv], [0, 0, 1.0]])
+        P = np.hstack([K @ rot, (-K @ rot @ src)[:, None]])
+        P /= P[2, 3]
+        for _ in range(50):
+            x, y, z = (r.uniform(-80, 80) for _ in range(3))
+            got = forward_project(m, x, y, z)
+            want = P @ np.array([x, y, z, 1.0])
+            assert np.allclose(got, want, rtol=1e-9, atol=1e-9)
+
+
+def test_geometry_validation():
+    with pytest.raises(pkg.ValidationError):
+        VolumeGeometry(0, 1.0, 0.0).validate()
+    with pytest.raises(pkg.ValidationError):
+        VolumeGeometry(8, -1.0, 0.0).validate()
+    c = small_config()
+    c.detector_width = 0
+    with pytest.raises(pkg.ValidationError, match="detector_width"):
+        make_circular_trajectory(c)
+    with pytest.raises(pkg.GeometryError):
+        dehomogenize(1.0, 1.0, 0.0)
+
+
+def test_centered_origin():
+    g = VolumeGeometry.centered(512, 0.5)
+    assert g.origin_mm == -127.75
+
+
+# --- file formats (restates proj/tests/test_dataset.cpp:33-128) ---------------
+
+def two_image_stack():
+    mats = np.zeros((2, 12))
+    mats[:, 11] = 1.0
+    mats[0, 0], mats[1, 0] = 1.0, 2.0
+    imgs = np.stack([np.full((3, 4), float(i), np.float32) for i in range(2)])
+    return pkg.ProjectionStack(VolumeGeometry(4, 1.0, -1.5), mats, imgs)
+
+
+def test_stack_file_size_and_roundtrip(tmp_path):
+    p = str(tmp_path / "s.cbps")
+    pkg.write_stack(p, two_image_stack())
+    header = 4 + 2 + 2 + 4 + 4 + 4 + 8 + 8 + 4
+    assert os.path.getsize(p) == header + 2 * (12 * 8 + 4 * 3 * 4)
+    s = pkg.read_stack(p)
+    p2 = str(tmp_path / "s2.cbps")
+    pkg.write_stack(p2, s)
+    assert open(p, "rb").read() == open(p2, "rb").read()
+
+
+def test_volume_file_roundtrip(tmp_path):
+    v = pkg.Volume(VolumeGeometry(3, 0.7, -2.0),
+                   np.arange(27, dtype=np.float32).reshape(3, 3, 3) * 0.5)
+    p = str(tmp_path / "v.cbpv")
+    pkg.write_volume(p, v)
+    assert os.path.getsize(p) == 4 + 2 + 2 + 4 + 8 + 8 + 27 * 4
+    w = pkg.read_volume(p)
+    assert np.array_equal(w.voxels, v.voxels) and w.geometry == v.geometry
+
+
+def test_file_corruption_cases(tmp_path):
+    p = str(tmp_path / "s.cbps")
+    pkg.write_stack(p, two_image_stack())
+    raw = bytearray(open(p, "rb").read())
+    bad = bytearray(raw)
+    bad[0:4] = b"SPBC"
+    open(p, "wb").write(bad)
+    with pytest.raises(pkg.FormatError):
+        pkg.read_stack(p)
+    bad = bytearray(raw)
+    bad[4] = 9
+    open(p, "wb").write(bad)
+    with pytest.raises(pkg.FormatError):
+        pkg.read_stack(p)
+    open(p, "wb").write(raw[:-7])
+    with pytest.raises(pkg.TruncatedError):
+        pkg.read_stack(p)
+    open(p, "wb").write(raw + b"\0")
+    with pytest.raises(pkg.FormatError):
+        pkg.read_stack(p)
+    with pytest.raises(pkg.IOError_):
+        pkg.read_stack(str(tmp_path / "missing.cbps"))
+
+
+# --- generator ---------------------------------------------------------------
+
+def test_splitmix64_known_values():
+    # splitmix64 reference outputs for seed 1234567
+    r = synth.SplitMix64(1234567)
+    assert [r.next_u64() for _ in range(3)] == [6457827717110365317, 3203168211198807973,
+                                                9817491932198370423]
+
+
+def test_generator_is_deterministic_and_border_heavy():
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=16, num_projections=3, width=156,
+                       height=120)
+    g1, m1, i1 = synth.make_inputs(cfg)
+    g2, m2, i2 = synth.make_inputs(cfg)
+    assert np.array_equal(m1, m2) and bool((i1 == i2).all())
+    # perturbed matrices keep the w(0) == 1 normalisation
+    for m in m1:
+        assert abs(forward_project(m, 0, 0, 0)[2] - 1.0) < 1e-12
+    im = i1.numpy()
+    assert np.abs(im[:, :, 0]).mean() > 1.2 * np.abs(im[:, :, 78]).mean()
+
+
+def test_baseline_config_arithmetic():
+    assert synth.CONFIGS[0].voxel_updates == 128 ** 3 * 496
+    assert synth.CONFIGS[2].voxel_updates == 512 ** 3 * 496
+    assert synth.CONFIGS[4].voxel_updates == 1024 ** 3 * 1440
+
+
+# --- the C ABI ----------------------------------------------------------------
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "conebeam_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(cbb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1401_3615_b200 import _lib
+
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(_lib.EXPORTS)
+
+
+def test_status_names_and_layout_without_gpu():
+    from paper_1401_3615_b200 import _lib
+
+    L = _lib.lib()
+    assert L.cbb_status_name(0) == b"ok"
+    assert L.cbb_status_name(5) == b"geometry error"
+    qp, qr, nb = pkg.packed_layout(1248, 960)
+    assert qp % 8 == 0 and qp >= 1248 + 3 and qr == 963 and nb == qp * qr * 16
+    with pytest.raises(pkg.ValidationError):
+        pkg.packed_layout(0, 10)
+
+
+def test_struct_layouts_match_header():
+    from paper_1401_3615_b200 import _lib
+
+    assert ctypes.sizeof(_lib.VolumeGeometryC) == 24
+    assert ctypes.sizeof(_lib.OptionsC) == 40
+    assert ctypes.sizeof(_lib.RunStatsC) == 8 * 4 + 8 * 2 + 8 + 8 * 8
