@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -143,13 +144,49 @@ cbb_options resolve_options(const cbb_options* o) {
 // cases of the IEEE division are then handled by the reference arithmetic).
 // ---------------------------------------------------------------------------
 
-bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_begin, int z_end) {
-    const float fa0 = 0.0f;
+// Smallest nonzero |O + i*MM| over i in [i0, i1), evaluated in float exactly
+// as the kernel does (0 when every coordinate is exactly zero).
+double min_nonzero_coord(float O, float MM, int i0, int i1) {
+    double m = 0.0;
+    for (int i = i0; i < i1; ++i) {
+        volatile float t = (float)i * MM;
+        volatile float c = O + t;
+        const double ac = std::fabs((double)c);
+        if (ac != 0.0 && (m == 0.0 || ac < m))
+            m = ac;
+    }
+    return m;
+}
+
+// Every nonzero partial sum of ((t1 + t2) + t3) + t4 is a multiple of the
+// smallest ulp among its nonzero float terms, so nonzero |u| >= 2^(e - 23)
+// with e the exponent of the smallest nonzero term. Requires |u| >= 2^-63.
+bool coordinate_sum_bounded(const float* af, const int idx[4], const double cmin[3]) {
+    double tmin = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        const double ak = std::fabs((double)af[idx[k]]);
+        if (ak == 0.0)
+            continue;
+        double t = k < 3 ? ak * cmin[k] * 0.5 : ak; // 0.5: product rounding
+        if (k < 3 && cmin[k] == 0.0)
+            continue;
+        if (tmin == 0.0 || t < tmin)
+            tmin = t;
+    }
+    return tmin == 0.0 || tmin >= 0x1p-40;
+}
+
+bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_begin, int z_end,
+                        const double cmin[3]) {
+    float af[12];
     for (int i = 0; i < 12; ++i) {
-        const float f = (float)a[i];
-        if (f == fa0 && std::signbit(f))
+        af[i] = (float)a[i];
+        if (af[i] == 0.0f && std::signbit(af[i]))
             return false;
     }
+    static const int urow[4] = {0, 3, 6, 9}, vrow[4] = {1, 4, 7, 10};
+    if (!coordinate_sum_bounded(af, urow, cmin) || !coordinate_sum_bounded(af, vrow, cmin))
+        return false;
     const int L = g.edge_voxels;
     const double lo = g.origin_mm;
     const double hi = g.origin_mm + (L - 1) * g.voxel_mm;
@@ -164,7 +201,7 @@ bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_beg
         const double w = wx * a[2] + wy * a[5] + wz * a[8] + a[11];
         const double scale = std::fabs(wx * a[2]) + std::fabs(wy * a[5]) +
                              std::fabs(wz * a[8]) + std::fabs(a[11]);
-        if (!(w > 1e-4 * scale) || !(w > 1e-30))
+        if (!(w > 1e-4 * scale) || !(w >= 0x1p-7) || !(w <= 0x1p7))
             return false;
         if (!(std::fabs(u / w) < 1e8) || !(std::fabs(v / w) < 1e8))
             return false;
@@ -187,14 +224,32 @@ void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaSt
     ++g_launches;
 }
 
-template <int MODE, bool GUARD>
-void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
+template <int R, int MODE, bool GUARD, int MINB>
+void launch_bp_r(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
     dim3 block(kBlockX, kBlockY);
     dim3 grid((args.L + kBlockX - 1) / kBlockX, (args.L + kBlockY - 1) / kBlockY,
-              (nz + kR - 1) / kR);
-    bp_kernel<kR, MODE, GUARD><<<grid, block, 0, st>>>(args, mats);
+              (nz + R - 1) / R);
+    bp_kernel<R, MODE, GUARD, MINB><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
+}
+
+// Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides).
+int bp_variant() {
+    const char* e = std::getenv("CBB_BP_VARIANT");
+    return e ? std::atoi(e) : 0;
+}
+
+template <int MODE, bool GUARD>
+void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
+    if (GUARD)
+        return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
+    switch (bp_variant()) {
+    case 1: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
+    case 2: return launch_bp_r<4, MODE, GUARD, 2>(args, mats, nz, st);
+    case 3: return launch_bp_r<4, MODE, GUARD, 3>(args, mats, nz, st);
+    default: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
+    }
 }
 
 // Launches ceil(count/batch) back-projection kernels over a slab. Returns the
@@ -219,19 +274,22 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.qpitchf = (float)qp;
     args.cell_bias = (float)(2 * qp + 2) + 8388608.0f;
     args.err = err;
+    args.neg_zero2 = 0x8000000080000000ull;
     uint64_t guarded_launches = 0;
     const int nz = z_end - z_begin;
     if (nz <= 0 || count <= 0)
         return 0;
+    const float Of = (float)g.origin_mm, MMf = (float)g.voxel_mm;
+    const double cxy = min_nonzero_coord(Of, MMf, 0, g.edge_voxels);
+    const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, z_begin, z_end)};
     for (int first = 0; first < count; first += opt.batch) {
         const int n = std::min(opt.batch, count - first);
         BpMats m;
         bool safe = true;
         for (int p = 0; p < n; ++p) {
             const double* a = mats + 12 * (size_t)(first + p);
-            for (int i = 0; i < 12; ++i)
-                m.a[p][i] = (float)a[i];
-            safe = safe && projection_is_safe(a, g, z_begin, z_end);
+            store_matrix(m.a[p], a);
+            safe = safe && projection_is_safe(a, g, z_begin, z_end, cmin);
         }
         if (!safe && !err)
             fail(CBB_ERR_INVALID,
