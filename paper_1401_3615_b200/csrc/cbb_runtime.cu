@@ -226,7 +226,7 @@ void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaSt
 
 template <int R, int MODE, bool GUARD, int MINB>
 void launch_bp_r(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
-    dim3 block(kBlockX, kBlockY);
+    dim3 block(kBlockX * kBlockY);
     dim3 grid((args.L + kBlockX - 1) / kBlockX, (args.L + kBlockY - 1) / kBlockY,
               (nz + R - 1) / R);
     bp_kernel<R, MODE, GUARD, MINB><<<grid, block, 0, st>>>(args, mats);
@@ -275,6 +275,7 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.cell_bias = (float)(2 * qp + 2) + 8388608.0f;
     args.err = err;
     args.neg_zero2 = 0x8000000080000000ull;
+    args.cull = opt.cull ? 1 : 0;
     uint64_t guarded_launches = 0;
     const int nz = z_end - z_begin;
     if (nz <= 0 || count <= 0)

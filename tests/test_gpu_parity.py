@@ -57,6 +57,25 @@ def test_batch_size_does_not_change_a_bit(cuda, batch):
     assert bits_equal(v, expected)
 
 
+def test_culling_is_exact(cuda):
+    g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
+    on, _ = gpu_reconstruct(g, mats, imgs, vol0, cull=True)
+    off, _ = gpu_reconstruct(g, mats, imgs, vol0, cull=False)
+    assert bits_equal(on, expected) and bits_equal(off, expected)
+
+
+def test_negative_zero_voxels_keep_reference_semantics(cuda, oracle):
+    # -0.0 + (+0) = +0 in the reference; culling must not skip that update
+    g, mats, imgs, vol0, _ = load_golden("mini_c0.npz")
+    v0 = vol0.copy()
+    v0[::2, ::3, :] = -0.0
+    ref = v0.copy()
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    for mode_cull in (True, False):
+        v, _ = gpu_reconstruct(g, mats, imgs, v0, cull=mode_cull)
+        assert bits_equal(v, ref)
+
+
 def test_per_projection_entry_point(cuda):
     # backproject_reference semantics, one call per projection
     g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
