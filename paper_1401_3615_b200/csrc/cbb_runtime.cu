@@ -224,12 +224,20 @@ void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaSt
     ++g_launches;
 }
 
-template <int R, int MODE, bool GUARD, int MINB>
-void launch_bp_r(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
+template <int R, int MODE, bool GUARD, int MINB, int SW = 0>
+void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
+    BpArgs args = a;
+    args.nbx = (args.L + kBlockX - 1) / kBlockX;
+    args.nby = (args.L + kBlockY - 1) / kBlockY;
+    args.nbz = (nz + R - 1) / R;
     dim3 block(kBlockX * kBlockY);
-    dim3 grid((args.L + kBlockX - 1) / kBlockX, (args.L + kBlockY - 1) / kBlockY,
-              (nz + R - 1) / R);
-    bp_kernel<R, MODE, GUARD, MINB><<<grid, block, 0, st>>>(args, mats);
+    dim3 grid(args.nbx, args.nby, args.nbz);
+    if (SW) {
+        const long long ns = (long long)((args.nbx + kSX - 1) / kSX) *
+                             ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
+        grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
+    }
+    bp_kernel<R, MODE, GUARD, MINB, SW><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -248,6 +256,7 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     case 1: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
     case 2: return launch_bp_r<4, MODE, GUARD, 2>(args, mats, nz, st);
     case 3: return launch_bp_r<4, MODE, GUARD, 3>(args, mats, nz, st);
+    case 4: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
     default: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
     }
 }

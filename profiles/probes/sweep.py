@@ -26,10 +26,11 @@ packed = torch.empty(n * nb, dtype=torch.uint8, device="cuda")
 vol = torch.empty((L, L, L), dtype=torch.float32, device="cuda")
 err = torch.zeros(1, dtype=torch.int32, device="cuda")
 ref = None
+BATCH = int(os.environ.get("SWEEP_BATCH", "32"))
 for mode in (pkg.MODE_EXACT, pkg.MODE_FAST):
     for v in variants:
         os.environ["CBB_BP_VARIANT"] = str(v)
-        opt = pkg.Options(mode=mode)
+        opt = pkg.Options(mode=mode, batch=BATCH)
 
         def step():
             vol.zero_()

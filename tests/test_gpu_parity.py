@@ -76,6 +76,23 @@ def test_negative_zero_voxels_keep_reference_semantics(cuda, oracle):
         assert bits_equal(v, ref)
 
 
+def test_cpp_adapter_with_reference_types(cuda):
+    """oracle/_ref/adapter_golden: the reference's own types and generators
+    (golden case) through include/conebeam_b200.hpp -> libconebeam_b200.so,
+    compared with the reference's reconstruct_reference (built here from
+    /root/reference; the binary travels with the snapshot)."""
+    import subprocess
+
+    import oracle as O
+
+    exe = O.os.path.join(O.HERE, "_ref", "adapter_golden")
+    if not O.os.path.exists(exe):
+        pytest.skip("adapter_golden not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "reference ab67551f9fba3780 b200 ab67551f9fba3780" in out.stdout
+
+
 def test_per_projection_entry_point(cuda):
     # backproject_reference semantics, one call per projection
     g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
