@@ -357,13 +357,12 @@ def run_ours(args):
         del packed
         torch.cuda.empty_cache()
         imgs_np = imgs_h.numpy()
-        vol_h = torch.zeros(((z1 - z0), L, L), dtype=torch.float32).pin_memory()
-        full = np.zeros((L, L, L), np.float32) if world == 1 else None
+        # the host volume (pinned): this rank's slab planes are written by the call
+        vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
+        buf = vol_h.numpy()
         e2e_opt = pkg.Options(batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
                               volume_is_zero=True, slab=(z0, z1))
-        buf = full if full is not None else np.zeros((L, L, L), np.float32)
-        for _ in range(1):
-            pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)
+        pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)  # warm-up
         if dist:
             dist.barrier()
         e2e_s = []

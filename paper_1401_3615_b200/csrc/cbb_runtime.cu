@@ -17,7 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -324,6 +326,70 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
 }
 
 // ---------------------------------------------------------------------------
+// Device buffer cache: repeated reconstructions (per-projection calls,
+// benchmark loops) reuse device buffers instead of paying cudaMalloc/cudaFree
+// (~ms for GB-sized slabs) per call. Blocks are reused when the cached block
+// is at least the request and at most twice its size.
+// ---------------------------------------------------------------------------
+
+class DevicePool {
+  public:
+    static DevicePool& get() {
+        static DevicePool p;
+        return p;
+    }
+
+    void* alloc(int device, size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto& fl = free_[device];
+            auto it = fl.lower_bound(bytes);
+            if (it != fl.end() && it->first <= 2 * bytes) {
+                void* p = it->second;
+                sizes_[p] = it->first;
+                fl.erase(it);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            trim(device);
+            e = cudaMalloc(&p, bytes);
+        }
+        check_cuda(e, "cudaMalloc");
+        std::lock_guard<std::mutex> lk(mu_);
+        sizes_[p] = bytes;
+        return p;
+    }
+
+    void release(int device, void* p) {
+        if (!p)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = sizes_.find(p);
+        if (it == sizes_.end())
+            return;
+        free_[device].emplace(it->second, p);
+        sizes_.erase(it);
+    }
+
+    void trim(int device) {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& kv : free_[device])
+            cudaFree(kv.second);
+        free_[device].clear();
+    }
+
+  private:
+    std::mutex mu_;
+    std::map<int, std::multimap<size_t, void*>> free_;
+    std::map<void*, size_t> sizes_;
+};
+
+// ---------------------------------------------------------------------------
 // Per-device worker: slab volume, raw/packed double buffers, streams, events.
 // ---------------------------------------------------------------------------
 
@@ -347,14 +413,15 @@ struct Worker {
         cudaSetDevice(device);
         cudaStreamSynchronize(copy);
         cudaStreamSynchronize(compute);
-        cudaFree(d_vol);
+        auto& pool = DevicePool::get();
+        pool.release(device, d_vol);
         for (int i = 0; i < 2; ++i) {
-            cudaFree(d_raw[i]);
-            cudaFree(d_packed[i]);
+            pool.release(device, d_raw[i]);
+            pool.release(device, d_packed[i]);
             cudaEventDestroy(h2d_done[i]);
             cudaEventDestroy(raw_free[i]);
         }
-        cudaFree(d_err);
+        pool.release(device, d_err);
         cudaEventDestroy(k_beg);
         cudaEventDestroy(k_end);
         cudaEventDestroy(c_beg);
@@ -363,6 +430,31 @@ struct Worker {
         cudaStreamDestroy(compute);
     }
 };
+
+// Host copy into pinned staging, split over a few threads for large blocks
+// (a single thread moves ~5-10 GB/s, below the PCIe H2D rate).
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kChunk = size_t(8) << 20;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 8), (bytes + kChunk - 1) / kChunk);
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (bytes + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t off = t * per;
+        if (off >= bytes)
+            break;
+        const size_t len = std::min(per, bytes - off);
+        pool.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len);
+        });
+    }
+    for (auto& th : pool)
+        th.join();
+}
 
 double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.0f;
@@ -426,16 +518,18 @@ struct Pipeline {
             for (int s = 0; s < 2; ++s) {
                 CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
-                CK(cudaMalloc(&w->d_raw[s], raw_bytes_per_proj * opt.batch));
-                CK(cudaMalloc(&w->d_packed[s], packed_bytes_per_proj * opt.batch));
+                w->d_raw[s] = static_cast<float*>(
+                    DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
+                w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
             }
             CK(cudaEventCreate(&w->k_beg));
             CK(cudaEventCreate(&w->k_end));
             CK(cudaEventCreate(&w->c_beg));
             CK(cudaEventCreate(&w->c_end));
             const size_t slab = plane * (w->z_end - w->z_begin);
-            CK(cudaMalloc(&w->d_vol, std::max<size_t>(slab, 1) * sizeof(float)));
-            CK(cudaMalloc(&w->d_err, sizeof(int)));
+            w->d_vol = static_cast<float*>(
+                DevicePool::get().alloc(w->device, std::max<size_t>(slab, 1) * sizeof(float)));
+            w->d_err = static_cast<int*>(DevicePool::get().alloc(w->device, sizeof(int)));
             CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
             CK(cudaEventRecord(w->c_beg, w->copy));
             if (initial_volume && !opt.volume_is_zero)
@@ -447,8 +541,6 @@ struct Pipeline {
             CK(cudaStreamWaitEvent(w->compute, w->c_end, 0));
             workers.push_back(std::move(w));
         }
-        for (int s = 0; s < 2; ++s)
-            CK(cudaHostAlloc(&h_stage[s], raw_bytes_per_proj * opt.batch, cudaHostAllocPortable));
         stage_mats.assign(12 * (size_t)opt.batch, 0.0);
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
@@ -491,7 +583,16 @@ struct Pipeline {
         }
     }
 
+    // Pinned staging for pageable sources, allocated on first use only.
+    void ensure_staging() {
+        for (int s = 0; s < 2; ++s)
+            if (!h_stage[s])
+                CK(cudaHostAlloc(&h_stage[s], raw_bytes_per_proj * opt.batch,
+                                 cudaHostAllocPortable));
+    }
+
     void stage_one(const float* img, const double* m) {
+        ensure_staging();
         if (stage_fill == 0)
             wait_slot(slot);
         std::memcpy(h_stage[slot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
@@ -523,8 +624,9 @@ struct Pipeline {
             if (pinned) {
                 issue(src, mats + 12 * (size_t)first, n);
             } else {
+                ensure_staging();
                 wait_slot(slot);
-                std::memcpy(h_stage[slot], src, raw_bytes_per_proj * n);
+                parallel_memcpy(h_stage[slot], src, raw_bytes_per_proj * n);
                 issue(h_stage[slot], mats + 12 * (size_t)first, n);
             }
         }
