@@ -1,0 +1,223 @@
+"""Multi-GPU z-slab reconstruction, one process per GPU (north_star (3)).
+
+Each rank owns a contiguous range of z-planes of the volume (voxel ownership
+is disjoint, every voxel keeps its projection order, so the result is
+bitwise that of one GPU). Projection batches are distributed with a
+broadcast over NCCL (NVLink / NVSwitch): batch b is uploaded from pinned host
+memory by rank b % N only and broadcast to the others, so each GPU's PCIe
+link carries 1/N of the host-to-device traffic and NVLink carries the rest.
+Slabs are copied to host memory at the end (no reduction).
+
+torch.distributed is the plumbing (process group, NCCL broadcast, streams);
+the compute is the C-ABI library (pack_device / backproject_device). The
+compute hooks can be replaced for host-side tests of the data flow (gloo,
+CPU tensors); the product default has no CPU path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from .geometry import VolumeGeometry, validate_matrices
+
+
+def equal_slabs(L: int, world: int) -> List[tuple]:
+    """Planes [L*r/N, L*(r+1)/N) per rank."""
+    return [(L * r // world, L * (r + 1) // world) for r in range(world)]
+
+
+def plane_work(geometry: VolumeGeometry, mats: np.ndarray, width: int, height: int,
+               samples: int = 16, planes_per_group: int = 8) -> np.ndarray:
+    """Estimated back-projection work per z-plane: the fraction of
+    (voxel, projection) pairs whose position lies in [-2, W) x [-2, H) (the
+    rest is culled as exactly zero), sampled on a samples x samples grid per
+    group of planes. Deterministic, float64, identical on every rank."""
+    L = geometry.edge_voxels
+    m = validate_matrices(mats)
+    idx = np.linspace(0, L - 1, samples)
+    wx = geometry.origin_mm + idx * geometry.voxel_mm
+    X, Y = np.meshgrid(wx, wx, indexing="xy")
+    X, Y = X.ravel(), Y.ravel()
+    groups = np.arange(0, L, planes_per_group)
+    work = np.zeros(L)
+    for g0 in groups:
+        zc = geometry.origin_mm + (g0 + (min(planes_per_group, L - g0) - 1) / 2) * geometry.voxel_mm
+        u = np.outer(m[:, 0], X) + np.outer(m[:, 3], Y) + (m[:, 6] * zc + m[:, 9])[:, None]
+        v = np.outer(m[:, 1], X) + np.outer(m[:, 4], Y) + (m[:, 7] * zc + m[:, 10])[:, None]
+        w = np.outer(m[:, 2], X) + np.outer(m[:, 5], Y) + (m[:, 8] * zc + m[:, 11])[:, None]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ix, iy = u / w, v / w
+        on = (ix > -2) & (ix < width) & (iy > -2) & (iy < height)
+        work[g0:g0 + planes_per_group] = on.mean() + 0.05  # + fixed per-voxel overhead
+    return work
+
+
+def balanced_slabs(work: np.ndarray, world: int) -> List[tuple]:
+    """Contiguous plane ranges with near-equal summed work (at least one
+    plane each when L >= world)."""
+    L = len(work)
+    c = np.concatenate([[0.0], np.cumsum(work)])
+    bounds = [0]
+    for r in range(1, world):
+        target = c[-1] * r / world
+        z = int(np.searchsorted(c, target))
+        z = max(bounds[-1] + 1, min(z, L - (world - r)))
+        bounds.append(z)
+    bounds.append(L)
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def batch_roots(count: int, batch: int, world: int) -> List[tuple]:
+    """(first, n, root) per batch: batch b is uploaded by rank b % world."""
+    out = []
+    for b, first in enumerate(range(0, count, batch)):
+        out.append((first, min(batch, count - first), b % world))
+    return out
+
+
+@dataclass
+class Hooks:
+    """Compute hooks: pack(raw (n,H,W), packed) and
+    backproject(vol_slab, z0, z1, packed, n, mats)."""
+    pack: Callable
+    backproject: Callable
+    packed_bytes: int
+
+
+def cuda_hooks(geometry: VolumeGeometry, width: int, height: int, options=None) -> Hooks:
+    from .backproject import backproject_device, pack_device, packed_layout
+
+    _, _, nb = packed_layout(width, height)
+
+    def pack(raw, packed):
+        pack_device(raw, packed)
+
+    def back(vol_slab, z0, z1, packed, n, mats, err):
+        backproject_device(vol_slab, geometry, z0, z1, packed, width, height, n, mats,
+                           options, err_flag=err)
+
+    return Hooks(pack, back, nb)
+
+
+class DistributedReconstructor:
+    """z-slab reconstruction across the ranks of a torch.distributed group.
+
+    reconstruct(host_imgs, mats) -> this rank's slab (host float32 array of
+    shape (z1 - z0, L, L)); host_imgs needs valid data only for the batches
+    this rank uploads (batch_roots)."""
+
+    def __init__(self, geometry: VolumeGeometry, width: int, height: int, batch: int = 32,
+                 slabs: Optional[Sequence[tuple]] = None, group=None, device=None,
+                 hooks: Optional[Hooks] = None, options=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.geometry = geometry
+        self.W, self.H = int(width), int(height)
+        self.batch = int(batch)
+        L = geometry.edge_voxels
+        self.slabs = list(slabs) if slabs is not None else equal_slabs(L, self.world)
+        assert len(self.slabs) == self.world
+        self.z0, self.z1 = self.slabs[self.rank]
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self.cuda = self.device.type == "cuda"
+        self.hooks = hooks or cuda_hooks(geometry, width, height, options)
+        nb = self.hooks.packed_bytes
+        self.raw = [torch.empty((self.batch, self.H, self.W), dtype=torch.float32,
+                                device=self.device) for _ in range(2)]
+        self.packed = [torch.empty(self.batch * nb, dtype=torch.uint8, device=self.device)
+                       for _ in range(2)]
+        self.vol = torch.zeros(((self.z1 - self.z0), L, L), dtype=torch.float32,
+                               device=self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.copy_stream = torch.cuda.Stream(self.device) if self.cuda else None
+
+    def _send(self, slot: int, host_imgs, first: int, n: int, root: int):
+        """Root uploads batch rows [first, first+n) into raw[slot]; broadcast."""
+        import torch
+
+        buf = self.raw[slot][:n]
+        if self.cuda:
+            cur = torch.cuda.current_stream(self.device)
+            self.copy_stream.wait_stream(cur)  # raw[slot] free (pack of batch b-2 done)
+            with torch.cuda.stream(self.copy_stream):
+                if self.rank == root:
+                    src = host_imgs[first:first + n]
+                    if not isinstance(src, torch.Tensor):
+                        src = torch.from_numpy(np.ascontiguousarray(src))
+                    buf.copy_(src, non_blocking=True)
+                if self.world > 1:
+                    return self.dist.broadcast(buf, src=root, group=self.group, async_op=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+                return ev
+        if self.rank == root:
+            src = host_imgs[first:first + n]
+            buf.copy_(src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src)))
+        if self.world > 1:
+            self.dist.broadcast(buf, src=root, group=self.group)
+        return None
+
+    def reconstruct(self, host_imgs, mats, initial_slab=None) -> np.ndarray:
+        import torch
+
+        m = validate_matrices(mats)
+        count = m.shape[0]
+        if initial_slab is not None:
+            self.vol.copy_(torch.as_tensor(np.ascontiguousarray(initial_slab)))
+        else:
+            self.vol.zero_()
+        self.err.zero_()
+        plan = batch_roots(count, self.batch, self.world)
+        pending = self._send(0, host_imgs, *plan[0]) if plan else None
+        for b, (first, n, root) in enumerate(plan):
+            slot = b & 1
+            nxt = None
+            if b + 1 < len(plan):
+                nxt = self._send(slot ^ 1, host_imgs, *plan[b + 1])
+            if self.cuda and pending is not None:
+                if isinstance(pending, torch.cuda.Event):
+                    torch.cuda.current_stream(self.device).wait_event(pending)
+                else:
+                    pending.wait()
+            self.hooks.pack(self.raw[slot][:n], self.packed[slot])
+            self.hooks.backproject(self.vol, self.z0, self.z1, self.packed[slot], n,
+                                   m[first:first + n], self.err)
+            pending = nxt
+        if int(self.err.item()) != 0:
+            from .errors import GeometryError
+            raise GeometryError("backprojection hit a voxel with w == 0")
+        out = torch.empty(self.vol.shape, dtype=torch.float32,
+                          pin_memory=self.cuda)
+        out.copy_(self.vol)
+        return out.numpy()
+
+    def gather(self, slab: np.ndarray, dst: int = 0) -> Optional[np.ndarray]:
+        """Collects every rank's slab into the full volume on rank `dst`
+        (host memory); other ranks return None."""
+        import torch
+
+        L = self.geometry.edge_voxels
+        t = torch.from_numpy(np.ascontiguousarray(slab)).to(self.device)
+        if self.world == 1:
+            return slab
+        sizes = [(z1 - z0) for z0, z1 in self.slabs]
+        full = [torch.empty((s, L, L), dtype=torch.float32, device=self.device)
+                for s in sizes] if self.rank == dst else None
+        if self.rank == dst:
+            for r in range(self.world):
+                if r == dst:
+                    full[r].copy_(t)
+                else:
+                    self.dist.recv(full[r], src=r, group=self.group)
+            return torch.cat(full).cpu().numpy()
+        self.dist.send(t, dst=dst, group=self.group)
+        return None

@@ -1,0 +1,118 @@
+"""CPU (gloo, world_size 2): host-side logic of the multi-GPU z-slab driver --
+slab plans, batch-root rotation, broadcast data flow, per-voxel projection
+order, slab gather. The compute hooks are an order-sensitive stub (no CUDA on
+this box); the CUDA hooks are exercised by the GPU tests and bench.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1401_3615_b200 import distributed as D
+from paper_1401_3615_b200 import synth
+from paper_1401_3615_b200.geometry import VolumeGeometry
+
+L, W, H, N, BATCH = 12, 7, 5, 11, 3
+
+
+def stub_hooks():
+    nb = W * H * 4
+
+    def pack(raw, packed):
+        n = raw.shape[0]
+        packed[: n * nb].copy_(raw.reshape(-1).view(torch.uint8))
+
+    def back(vol, z0, z1, packed, n, mats, err):
+        imgs = packed[: n * nb].view(torch.float32).reshape(n, H, W)
+        z = torch.arange(z0, z1, dtype=torch.float32).reshape(-1, 1, 1)
+        for j in range(n):
+            # order-sensitive update: acc = 0.5*acc + f(projection, z, matrix)
+            f = imgs[j].sum() * (z + 1.0) + float(mats[j][0])
+            vol.mul_(0.5).add_(f)
+
+    return D.Hooks(pack, back, nb)
+
+
+def sequential_reference(imgs, mats):
+    vol = torch.zeros((L, L, L))
+    z = torch.arange(0, L, dtype=torch.float32).reshape(-1, 1, 1)
+    for j in range(N):
+        vol.mul_(0.5).add_(torch.from_numpy(imgs[j]).sum() * (z + 1.0) + float(mats[j][0]))
+    return vol.numpy()
+
+
+def data():
+    r = np.random.default_rng(5)
+    imgs = r.standard_normal((N, H, W)).astype(np.float32)
+    mats = r.standard_normal((N, 12))
+    return imgs, mats
+
+
+def worker(rank, world, port, slabs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        imgs, mats = data()
+        # each rank only holds the batches it uploads; the rest is garbage
+        mine = np.full_like(imgs, np.nan)
+        for first, n, root in D.batch_roots(N, BATCH, world):
+            if root == rank:
+                mine[first:first + n] = imgs[first:first + n]
+        rec = D.DistributedReconstructor(VolumeGeometry.centered(L, 1.0), W, H, batch=BATCH,
+                                         slabs=slabs, device="cpu", hooks=stub_hooks())
+        slab = rec.reconstruct(torch.from_numpy(mine), mats)
+        full = rec.gather(slab)
+        if rank == 0:
+            q.put(full)
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("slabs", [None, [(0, 3), (3, L)]])
+def test_two_ranks_match_sequential(slabs):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, slabs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    imgs, mats = data()
+    ref = sequential_reference(imgs, mats)
+    assert np.array_equal(full, ref)
+
+
+def test_slab_plans():
+    assert D.equal_slabs(10, 3) == [(0, 3), (3, 6), (6, 10)]
+    roots = D.batch_roots(100, 32, 3)
+    assert [r for _, _, r in roots] == [0, 1, 2, 0]
+    assert sum(n for _, n, _ in roots) == 100
+    cfg = synth.CONFIGS[2]
+    mats = synth.perturbed_matrices(cfg)
+    g = cfg.geometry
+    work = D.plane_work(g, mats[::8], cfg.width, cfg.height)
+    assert work.shape == (512,)
+    # centre planes see the detector from every angle, the top/bottom less
+    assert work[256] > work[0] and work[256] > work[511]
+    for world in (2, 4, 8):
+        sl = D.balanced_slabs(work, world)
+        assert sl[0][0] == 0 and sl[-1][1] == 512
+        assert all(a < b for a, b in sl) and all(sl[i][1] == sl[i + 1][0] for i in range(world - 1))
+        per = [work[a:b].sum() for a, b in sl]
+        assert max(per) / (sum(per) / world) < 1.05
+        eq = [work[a:b].sum() for a, b in D.equal_slabs(512, world)]
+        assert max(per) <= max(eq)
