@@ -283,7 +283,7 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.Wf = (float)W;
     args.Hf = (float)H;
     args.qpitchf = (float)qp;
-    args.cell_bias = (float)(2 * qp + 2) + 8388608.0f;
+    args.cell_bias = (float)(kPad * qp + kPad) + 8388608.0f;
     args.err = err;
     args.neg_zero2 = 0x8000000080000000ull;
     args.cull = opt.cull ? 1 : 0;

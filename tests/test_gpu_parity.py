@@ -50,7 +50,7 @@ def test_reference_fixtures_bitwise(cuda, name):
         assert st["guarded_batches"] > 0  # w changes sign: guarded kernel ran
 
 
-@pytest.mark.parametrize("batch", [1, 5, 64])
+@pytest.mark.parametrize("batch", [1, 5, 32])
 def test_batch_size_does_not_change_a_bit(cuda, batch):
     g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
     v, _ = gpu_reconstruct(g, mats, imgs, vol0, batch=batch)
