@@ -244,7 +244,9 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     ++g_launches;
 }
 
-// Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides).
+// Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides):
+// 0 = R 8 voxels/thread, 3 blocks/SM (default, measured best on config 2);
+// 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with super-tile order.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -255,11 +257,10 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     if (GUARD)
         return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
     switch (bp_variant()) {
-    case 1: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
-    case 2: return launch_bp_r<4, MODE, GUARD, 2>(args, mats, nz, st);
-    case 3: return launch_bp_r<4, MODE, GUARD, 3>(args, mats, nz, st);
-    case 4: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
-    default: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
+    case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
+    case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
+    case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
+    default: return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
     }
 }
 
