@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the other-mode and 1024^3 secondary measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU seconds for the cpu_baseline sample")
@@ -324,9 +326,17 @@ def run_ours(args):
     achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
     sm_load = clocks.get("sm_mhz") or sm_max
     hbm_bytes = 8 * (z1 - z0) * L * L + args.batch * nb  # volume rmw + packed inputs
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        rec = json.load(open(tpath)).get(f"{cfg.name}/{args.mode}")
+        if rec and world == 1:
+            traffic = rec["dram_bytes_per_launch"]
+            traffic_src = f"profiles/{rec['source']} (ncu --set full, one launch)"
     roofline = {
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 3),
-        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
+        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
+        "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(hbm_bytes),
         "peak_basis": f"{nsm} SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, "
                       f"{peak_src} peaks file); 34 algorithmic FP32 ops per voxel update",
         "frac_at_load_clock": round(achieved / (nsm * 128 * sm_load * 1e6 / 1e12), 4),
@@ -358,6 +368,56 @@ def run_ours(args):
         "clocks": clocks,
         "roofline": roofline,
     }
+
+    # secondary device-resident measurements (same projections, same packed
+    # buffer): the other arithmetic mode on this workload, and the 1024^3
+    # volume of config 3 (configs 0-3 share the scan)
+    if not args.no_secondary:
+        def measure(geom, mode_id, steps, slab):
+            zz0, zz1 = slab
+            LL = geom.edge_voxels
+            v2 = torch.empty(((zz1 - zz0), LL, LL), dtype=torch.float32, device=dev)
+            o2 = pkg.Options(batch=args.batch, mode=mode_id)
+
+            def st2():
+                v2.zero_()
+                pkg.pack_device(imgs, packed, stream)
+                pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream)
+            for _ in range(2):
+                st2()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(steps):
+                st2()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / steps
+            if dist:
+                t = torch.tensor([ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            del v2
+            return {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
+                    "ms_per_step": round(ms, 3)}
+
+        other = "fast" if args.mode == "exact" else "exact"
+        sec = [dict(workload=cfg.name, mode=other,
+                    **measure(g, pkg.MODE_FAST if other == "fast" else pkg.MODE_EXACT,
+                              args.steps, (z0, z1)))]
+        if args.config != 3 and cfg.width == synth.CONFIGS[3].width:
+            g3 = synth.CONFIGS[3].geometry
+            if world > 1:
+                from paper_1401_3615_b200.distributed import balanced_slabs, plane_work
+                sl3 = balanced_slabs(plane_work(g3, mats, W, H), world)[rank]
+            else:
+                sl3 = (0, g3.edge_voxels)
+            sec.append(dict(workload=synth.CONFIGS[3].name, mode=args.mode,
+                            **measure(g3, mode, 3, sl3)))
+        line["secondary"] = sec
+        torch.cuda.empty_cache()
 
     # e2e through the public host API: pinned host projections -> host volume
     if not args.no_e2e:

@@ -4,7 +4,7 @@
 # 3) one --set full capture of the back-projection kernel.
 set -u
 TAG=$1; shift
-ARGS="--steps 2 --warmup 3 --no-e2e --no-cpu-baseline $*"
+ARGS="--steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary $*"
 mkdir -p gpurun_out
 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain_$TAG.log; exit 1; }
 tail -1 gpurun_out/plain_$TAG.log

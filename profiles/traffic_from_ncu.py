@@ -1,0 +1,27 @@
+#!/usr/bin/env python
+"""Writes profiles/ncu_traffic.json from an ncu --set full report of one
+bp_kernel launch: dram__bytes_read.sum + dram__bytes_write.sum per launch
+(bench.py reports it as roofline.traffic)."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, workload, mode = sys.argv[1], sys.argv[2], sys.argv[3]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                     check=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+d = {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+tot = 0.0
+for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    u, v = d[k]
+    tot += float(v) * scale[u]
+path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json")
+data = json.load(open(path)) if os.path.exists(path) else {}
+data[f"{workload}/{mode}"] = {"dram_bytes_per_launch": tot, "kernel": d.get("Kernel Name", ("", ""))[1],
+                              "source": os.path.basename(rep)}
+json.dump(data, open(path, "w"), indent=1)
+print(data)
