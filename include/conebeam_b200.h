@@ -81,6 +81,9 @@ typedef struct cbb_options {
     int32_t volume_is_zero;    /* caller promises the input volume is all +0: skip its upload */
     int32_t slab_begin;        /* z-planes [slab_begin, slab_end) of the volume to update; */
     int32_t slab_end;          /* 0, 0 = all planes (one process per GPU drives one slab) */
+    int32_t ramp_filter;       /* 1: projections are raw line integrals; apply the FDK row-wise
+                                  Shepp-Logan ramp filter on the GPU before back-projecting */
+    double filter_pixel_mm;    /* detector pixel pitch tau of the ramp filter (mm) */
 } cbb_options;
 
 void cbb_options_defaults(cbb_options* options);
@@ -156,6 +159,14 @@ cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* ge
                                   int32_t width, int32_t height, int32_t count,
                                   const double* mats, const cbb_options* options,
                                   int32_t* err_flag, void* stream);
+
+/* FDK filtering step (upstream of the back-projection; the reference consumes
+ * pre-filtered data): row-wise Shepp-Logan ramp filter
+ * h[n] = -2/(pi^2 tau (4n^2-1)) as a linear convolution (zero-padded float64
+ * FFT, length >= 2W), rounded to float32. raw/out: count*height*width floats
+ * on the device (may alias). Enqueued on stream. */
+cbb_status cbb_ramp_filter_device(const float* raw, float* out, int32_t width, int32_t height,
+                                  int32_t count, double pixel_mm, void* stream);
 
 /* Number of kernel launches the last cbb_backproject_device / cbb_pack_device
  * calls on this thread issued (for the bench's gpu_launches count). */

@@ -20,7 +20,7 @@ EXPORTS = (
     "cbb_options_defaults", "cbb_backproject", "cbb_reconstruct",
     "cbb_session_create", "cbb_session_backproject", "cbb_session_finish",
     "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
-    "cbb_backproject_device", "cbb_launch_count",
+    "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
 )
 
 
@@ -33,7 +33,8 @@ class OptionsC(C.Structure):
     _fields_ = [("num_gpus", C.c_int32), ("device_ids", C.POINTER(C.c_int32)),
                 ("batch", C.c_int32), ("mode", C.c_int32), ("cull", C.c_int32),
                 ("volume_is_zero", C.c_int32), ("slab_begin", C.c_int32),
-                ("slab_end", C.c_int32)]
+                ("slab_end", C.c_int32), ("ramp_filter", C.c_int32),
+                ("filter_pixel_mm", C.c_double)]
 
 
 class RunStatsC(C.Structure):
@@ -92,6 +93,9 @@ def _declare(L) -> None:
     L.cbb_backproject_device.argtypes = [_VP, C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32,
                                          _VP, C.c_int32, C.c_int32, C.c_int32, _VP,
                                          C.POINTER(OptionsC), _VP, _VP]
+    L.cbb_ramp_filter_device.restype = C.c_int
+    L.cbb_ramp_filter_device.argtypes = [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                         _VP]
     L.cbb_launch_count.restype = C.c_uint64
     L.cbb_launch_count.argtypes = []
 

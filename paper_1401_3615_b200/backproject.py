@@ -44,6 +44,7 @@ class Options:
     cull: bool = True
     volume_is_zero: bool = False
     slab: Optional[Sequence[int]] = None  # (z_begin, z_end) planes to update; None = all
+    ramp_filter_pixel_mm: Optional[float] = None  # set: inputs are raw line integrals, FDK-filter on GPU
 
     def to_c(self):
         o = _lib.OptionsC()
@@ -61,6 +62,9 @@ class Options:
         o.volume_is_zero = int(bool(self.volume_is_zero))
         if self.slab is not None:
             o.slab_begin, o.slab_end = int(self.slab[0]), int(self.slab[1])
+        if self.ramp_filter_pixel_mm is not None:
+            o.ramp_filter = 1
+            o.filter_pixel_mm = float(self.ramp_filter_pixel_mm)
         return o, keep
 
 
@@ -253,6 +257,22 @@ def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: 
         packed.data_ptr() + int(first) * nb, int(width), int(height), int(count), _ptr(m),
         C.byref(oc), None if err_flag is None else err_flag.data_ptr(),
         C.c_void_p(s.cuda_stream)))
+
+
+def ramp_filter_device(raw, out, pixel_mm: float, stream=None) -> None:
+    """FDK row-wise Shepp-Logan ramp filter on the GPU (cbb_ramp_filter_device):
+    raw, out: contiguous CUDA float32 tensors (N, H, W) (may be the same)."""
+    import torch
+
+    for t in (raw, out):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.dim() == 3):
+            raise ValidationError("ramp_filter_device: contiguous CUDA float32 (N, H, W) tensors")
+    if raw.shape != out.shape:
+        raise ValidationError("ramp_filter_device: shapes differ")
+    n, h, w = raw.shape
+    s = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    _lib.check(_lib.lib().cbb_ramp_filter_device(raw.data_ptr(), out.data_ptr(), w, h, n,
+                                                 float(pixel_mm), C.c_void_p(s.cuda_stream)))
 
 
 def launch_count() -> int:

@@ -30,6 +30,7 @@
 
 #include "../../include/conebeam_b200.h"
 #include "bp_kernels.cuh"
+#include "ramp_filter.cuh"
 
 namespace cbb {
 
@@ -131,6 +132,8 @@ cbb_options resolve_options(const cbb_options* o) {
         fail(CBB_ERR_INVALID, "options: num_gpus must be >= 0");
     if (r.slab_begin < 0 || r.slab_end < 0 || (r.slab_end != 0 && r.slab_end <= r.slab_begin))
         fail(CBB_ERR_INVALID, "options: bad slab [%d, %d)", r.slab_begin, r.slab_end);
+    if (r.ramp_filter && !(r.filter_pixel_mm > 0.0 && std::isfinite(r.filter_pixel_mm)))
+        fail(CBB_ERR_INVALID, "options: ramp filter needs a positive filter_pixel_mm");
     return r;
 }
 
@@ -566,6 +569,9 @@ struct Pipeline {
                 CK(cudaEventRecord(w->k_beg, w->compute));
                 w->started = true;
             }
+            if (opt.ramp_filter)
+                ramp_filter_device(w->d_raw[slot], w->d_raw[slot], W, H, n, opt.filter_pixel_mm,
+                                   w->compute);
             launch_pack(w->d_raw[slot], W, H, n, w->d_packed[slot], w->compute);
             CK(cudaEventRecord(w->raw_free[slot], w->compute));
             w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end,
@@ -745,6 +751,8 @@ void cbb_options_defaults(cbb_options* o) {
     o->volume_is_zero = 0;
     o->slab_begin = 0;
     o->slab_end = 0;
+    o->ramp_filter = 0;
+    o->filter_pixel_mm = 0.0;
 }
 
 cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int32_t* qrows,
@@ -757,6 +765,22 @@ cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int
             *qrows = quad_rows(height);
         if (bytes)
             *bytes = (int64_t)quad_pitch_cells(width) * quad_rows(height) * 16;
+    });
+}
+
+cbb_status cbb_ramp_filter_device(const float* raw, float* out, int32_t width, int32_t height,
+                                  int32_t count, double pixel_mm, void* stream) {
+    return guarded([&] {
+        if (!raw || !out || count < 0)
+            fail(CBB_ERR_INVALID, "cbb_ramp_filter_device: null argument");
+        if (width < 1 || height < 1)
+            fail(CBB_ERR_INVALID, "ProjectionImage: dimensions must be >= 1");
+        if (!(pixel_mm > 0.0) || !std::isfinite(pixel_mm))
+            fail(CBB_ERR_INVALID, "cbb_ramp_filter_device: pixel_mm must be positive");
+        if (count == 0)
+            return;
+        ramp_filter_device(raw, out, width, height, count, pixel_mm,
+                           static_cast<cudaStream_t>(stream));
     });
 }
 
