@@ -399,9 +399,16 @@ def run_ours(args):
                 t = torch.tensor([ms], device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
+            res = {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
+                   "ms_per_step": round(ms, 3)}
+            if geom is g and mode_id != mode:
+                # full-size agreement of the two modes on the GPU (exact mode is
+                # bitwise the reference's result, see tests/test_gpu_parity.py)
+                dff = pkg.compare_volumes_device(v2, vol)
+                res["vs_exact" if mode_id == pkg.MODE_FAST else "vs_fast"] = {
+                    k: dff[k] for k in ("rel_l2", "max_abs_over_range", "bitwise_different")}
             del v2
-            return {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
-                    "ms_per_step": round(ms, 3)}
+            return res
 
         other = "fast" if args.mode == "exact" else "exact"
         sec = [dict(workload=cfg.name, mode=other,

@@ -168,6 +168,23 @@ cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* ge
 cbb_status cbb_ramp_filter_device(const float* raw, float* out, int32_t width, int32_t height,
                                   int32_t count, double pixel_mm, void* stream);
 
+/* Volume comparison on the device: quality_metrics (proj/src/bench.cpp:65-82),
+ * max_relative_error (:92-102) and the north_star parity figures. */
+typedef struct cbb_volume_diff {
+    double mse;                /* mean (t - r)^2 */
+    double psnr_db;            /* 10 log10(max_ref^2 / mse); +inf when mse == 0 */
+    double max_relative_error; /* max |t - r| / (|r| + denom_floor) */
+    double rel_l2;             /* ||t - r||_2 / ||r||_2 */
+    double max_abs;            /* max |t - r| */
+    double ref_min, ref_max;
+    double max_abs_over_range; /* max_abs / (ref_max - ref_min) */
+    uint64_t bitwise_different;
+} cbb_volume_diff;
+
+/* test, ref: n floats each on the device. Synchronous on stream. */
+cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64_t n,
+                                      double denom_floor, cbb_volume_diff* out, void* stream);
+
 /* Number of kernel launches the last cbb_backproject_device / cbb_pack_device
  * calls on this thread issued (for the bench's gpu_launches count). */
 uint64_t cbb_launch_count(void);

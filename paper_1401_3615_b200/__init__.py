@@ -4,6 +4,7 @@ Drop-in for the reference's hot path (proj/src/kernel_ref.cpp:5-38,
 proj/src/kernel_opt.cpp:658-716) through the C ABI in include/conebeam_b200.h.
 """
 from .backproject import (MODE_EXACT, MODE_FAST, Options, Session, backproject,
+                          compare_volumes_device,
                           backproject_device, device_count, launch_count, pack_device,
                           packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays)
 from .dataset import ProjectionStack, Volume, read_stack, read_volume, write_stack, write_volume
@@ -14,6 +15,7 @@ from .geometry import (TrajectoryConfig, VolumeGeometry, dehomogenize, forward_p
 
 __all__ = [
     "MODE_EXACT", "MODE_FAST", "Options", "Session", "backproject", "backproject_device",
+    "compare_volumes_device",
     "device_count", "launch_count", "pack_device", "packed_layout", "ramp_filter_device", "reconstruct",
     "reconstruct_arrays", "ProjectionStack", "Volume", "read_stack", "read_volume",
     "write_stack", "write_volume", "ConebeamError", "FormatError", "GeometryError",

@@ -21,6 +21,7 @@ EXPORTS = (
     "cbb_session_create", "cbb_session_backproject", "cbb_session_finish",
     "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
     "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
+    "cbb_compare_volumes_device",
 )
 
 
@@ -51,6 +52,17 @@ class RunStatsC(C.Structure):
             "guarded_batches": int(self.guarded_batches), "num_gpus": int(self.num_gpus),
             "per_gpu_kernel_seconds": list(self.per_gpu_kernel_seconds)[: max(self.num_gpus, 0)],
         }
+
+
+class VolumeDiffC(C.Structure):
+    _fields_ = [("mse", C.c_double), ("psnr_db", C.c_double),
+                ("max_relative_error", C.c_double), ("rel_l2", C.c_double),
+                ("max_abs", C.c_double), ("ref_min", C.c_double), ("ref_max", C.c_double),
+                ("max_abs_over_range", C.c_double), ("bitwise_different", C.c_uint64)]
+
+    def to_dict(self) -> dict:
+        return {k: (int(getattr(self, k)) if k == "bitwise_different" else getattr(self, k))
+                for k, _ in self._fields_}
 
 
 _lock = threading.Lock()
@@ -96,6 +108,9 @@ def _declare(L) -> None:
     L.cbb_ramp_filter_device.restype = C.c_int
     L.cbb_ramp_filter_device.argtypes = [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                          _VP]
+    L.cbb_compare_volumes_device.restype = C.c_int
+    L.cbb_compare_volumes_device.argtypes = [_VP, _VP, C.c_int64, C.c_double,
+                                             C.POINTER(VolumeDiffC), _VP]
     L.cbb_launch_count.restype = C.c_uint64
     L.cbb_launch_count.argtypes = []
 

@@ -275,6 +275,25 @@ def ramp_filter_device(raw, out, pixel_mm: float, stream=None) -> None:
                                                  float(pixel_mm), C.c_void_p(s.cuda_stream)))
 
 
+def compare_volumes_device(test, ref, denom_floor: float = 1e-6, stream=None) -> dict:
+    """quality_metrics / max_relative_error of the reference harness
+    (proj/src/bench.cpp:65-102) plus relL2, max|d|/range and the count of
+    bitwise-different voxels, computed on the GPU (cbb_compare_volumes_device)."""
+    import torch
+
+    for t in (test, ref):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValidationError("compare_volumes_device: contiguous CUDA float32 tensors")
+    if test.numel() != ref.numel() or test.numel() == 0:
+        raise ValidationError("compare_volumes_device: sizes differ or empty")
+    s = stream if stream is not None else torch.cuda.current_stream(test.device)
+    out = _lib.VolumeDiffC()
+    _lib.check(_lib.lib().cbb_compare_volumes_device(test.data_ptr(), ref.data_ptr(),
+                                                     test.numel(), float(denom_floor),
+                                                     C.byref(out), C.c_void_p(s.cuda_stream)))
+    return out.to_dict()
+
+
 def launch_count() -> int:
     return int(_lib.lib().cbb_launch_count())
 

@@ -31,6 +31,7 @@
 #include "../../include/conebeam_b200.h"
 #include "bp_kernels.cuh"
 #include "ramp_filter.cuh"
+#include "metrics.cuh"
 
 namespace cbb {
 
@@ -765,6 +766,50 @@ cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int
             *qrows = quad_rows(height);
         if (bytes)
             *bytes = (int64_t)quad_pitch_cells(width) * quad_rows(height) * 16;
+    });
+}
+
+cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64_t n,
+                                      double denom_floor, cbb_volume_diff* out, void* stream) {
+    return guarded([&] {
+        if (!test || !ref || !out || n < 1)
+            fail(CBB_ERR_INVALID, "cbb_compare_volumes_device: null or empty argument");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        auto* part = static_cast<MetricPartial*>(
+            DevicePool::get().alloc(dev, sizeof(MetricPartial) * kMetricBlocks));
+        metrics_partial<<<kMetricBlocks, kMetricThreads, 0, st>>>(test, ref, n, denom_floor, part);
+        ++g_launches;
+        std::vector<MetricPartial> h(kMetricBlocks);
+        const cudaError_t e1 = cudaGetLastError();
+        const cudaError_t e2 = cudaMemcpyAsync(h.data(), part, sizeof(MetricPartial) * kMetricBlocks,
+                                               cudaMemcpyDeviceToHost, st);
+        const cudaError_t e3 = cudaStreamSynchronize(st);
+        DevicePool::get().release(dev, part);
+        CK(e1);
+        CK(e2);
+        CK(e3);
+        double ssd = 0, ssr = 0, mabs = 0, mrel = 0, rmin = DBL_MAX, rmax = -DBL_MAX;
+        uint64_t nd = 0;
+        for (const auto& p : h) { // fixed order: deterministic
+            ssd += p.sum_sq_diff;
+            ssr += p.sum_sq_ref;
+            mabs = std::max(mabs, p.max_abs);
+            mrel = std::max(mrel, p.max_rel);
+            rmin = std::min(rmin, p.ref_min);
+            rmax = std::max(rmax, p.ref_max);
+            nd += p.bit_diff;
+        }
+        out->mse = ssd / (double)n;
+        out->psnr_db = out->mse == 0.0 ? INFINITY : 10.0 * std::log10(rmax * rmax / out->mse);
+        out->max_relative_error = mrel;
+        out->rel_l2 = ssr > 0.0 ? std::sqrt(ssd / ssr) : (ssd > 0.0 ? INFINITY : 0.0);
+        out->max_abs = mabs;
+        out->ref_min = rmin;
+        out->ref_max = rmax;
+        out->max_abs_over_range = rmax > rmin ? mabs / (rmax - rmin) : (mabs > 0 ? INFINITY : 0.0);
+        out->bitwise_different = nd;
     });
 }
 

@@ -51,6 +51,32 @@ def test_ramp_filter_matches_numpy(cuda):
     assert np.array_equal(t.cpu().numpy(), got)
 
 
+def test_compare_volumes_device_matches_numpy(cuda):
+    """GPU volume metrics vs the reference harness definitions
+    (proj/src/bench.cpp:65-102) computed in numpy float64."""
+    import torch
+
+    r = np.random.default_rng(3)
+    ref = r.standard_normal(100003).astype(np.float32)
+    test = (ref + r.standard_normal(ref.size).astype(np.float32) * 1e-3).astype(np.float32)
+    test[::7] = ref[::7]
+    got = pkg.compare_volumes_device(torch.from_numpy(test).cuda(), torch.from_numpy(ref).cuda(),
+                                     denom_floor=1e-6)
+    d = test.astype(np.float64) - ref
+    mse = np.mean(d * d)
+    assert got["mse"] == pytest.approx(mse, rel=1e-12)
+    assert got["psnr_db"] == pytest.approx(10 * np.log10(float(ref.max()) ** 2 / mse), rel=1e-12)
+    assert got["max_relative_error"] == pytest.approx(
+        np.max(np.abs(d) / (np.abs(ref.astype(np.float64)) + 1e-6)), rel=1e-12)
+    assert got["rel_l2"] == pytest.approx(np.linalg.norm(d) / np.linalg.norm(ref.astype(np.float64)),
+                                          rel=1e-9)
+    assert got["max_abs_over_range"] == pytest.approx(
+        np.abs(d).max() / (float(ref.max()) - float(ref.min())), rel=1e-12)
+    assert got["bitwise_different"] == int(np.sum(test.view(np.uint32) != ref.view(np.uint32)))
+    same = pkg.compare_volumes_device(torch.from_numpy(ref).cuda(), torch.from_numpy(ref).cuda())
+    assert same["bitwise_different"] == 0 and same["mse"] == 0 and same["psnr_db"] == float("inf")
+
+
 def test_filtered_pipeline_equals_backprojecting_filtered_data(cuda, oracle):
     import torch
 
