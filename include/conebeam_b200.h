@@ -119,6 +119,31 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry,
                            const cbb_options* options /* nullable */,
                            cbb_run_stats* stats /* nullable */);
 
+/* ---- streaming from a CBPS stack file ------------------------------------ */
+
+/* Header of a CBPS stack file (proj/include/conebeam/dataset.hpp:62-72) --
+ * the counterpart of cb_stack_read + cb_stack_get_info (capi.h:57-73) without
+ * loading the projections. Same error statuses as read_stack
+ * (proj/src/dataset.cpp:181-212): IO, FORMAT (magic, version, trailing bytes),
+ * TRUNCATED. */
+typedef struct cbb_stack_file_info {
+    int32_t edge_voxels;
+    double voxel_mm;
+    double origin_mm;
+    int32_t count;
+    int32_t width;
+    int32_t height;
+} cbb_stack_file_info;
+
+cbb_status cbb_stack_file_query(const char* path, cbb_stack_file_info* out);
+
+/* Reconstructs a CBPS file into vol (L^3 floats, accumulated like
+ * cbb_reconstruct), streaming the projection records from disk into pinned
+ * double buffers overlapped with the device work; memory use is independent
+ * of the projection count. Non-finite pixels -> CBB_ERR_INVALID. */
+cbb_status cbb_reconstruct_file(float* vol, const char* path, const cbb_options* options,
+                                cbb_run_stats* stats);
+
 /* ---- streaming session (RabbitCT-style per-projection module) ------------ */
 
 typedef struct cbb_session_s cbb_session;

@@ -6,7 +6,8 @@ proj/src/kernel_opt.cpp:658-716) through the C ABI in include/conebeam_b200.h.
 from .backproject import (MODE_EXACT, MODE_FAST, Options, Session, backproject,
                           compare_volumes_device,
                           backproject_device, device_count, launch_count, pack_device,
-                          packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays)
+                          packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays,
+                          reconstruct_file, stack_file_info)
 from .dataset import ProjectionStack, Volume, read_stack, read_volume, write_stack, write_volume
 from .errors import (ConebeamError, FormatError, GeometryError, InternalError, IOError_,
                      OutOfMemoryError, TruncatedError, ValidationError)
@@ -17,7 +18,7 @@ __all__ = [
     "MODE_EXACT", "MODE_FAST", "Options", "Session", "backproject", "backproject_device",
     "compare_volumes_device",
     "device_count", "launch_count", "pack_device", "packed_layout", "ramp_filter_device", "reconstruct",
-    "reconstruct_arrays", "ProjectionStack", "Volume", "read_stack", "read_volume",
+    "reconstruct_arrays", "reconstruct_file", "stack_file_info", "ProjectionStack", "Volume", "read_stack", "read_volume",
     "write_stack", "write_volume", "ConebeamError", "FormatError", "GeometryError",
     "InternalError", "IOError_", "OutOfMemoryError", "TruncatedError", "ValidationError",
     "TrajectoryConfig", "VolumeGeometry", "dehomogenize", "forward_project",

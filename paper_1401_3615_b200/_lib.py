@@ -21,8 +21,13 @@ EXPORTS = (
     "cbb_session_create", "cbb_session_backproject", "cbb_session_finish",
     "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
     "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
-    "cbb_compare_volumes_device",
+    "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
 )
+
+
+class StackFileInfoC(C.Structure):
+    _fields_ = [("edge_voxels", C.c_int32), ("voxel_mm", C.c_double), ("origin_mm", C.c_double),
+                ("count", C.c_int32), ("width", C.c_int32), ("height", C.c_int32)]
 
 
 class VolumeGeometryC(C.Structure):
@@ -108,6 +113,11 @@ def _declare(L) -> None:
     L.cbb_ramp_filter_device.restype = C.c_int
     L.cbb_ramp_filter_device.argtypes = [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                          _VP]
+    L.cbb_stack_file_query.restype = C.c_int
+    L.cbb_stack_file_query.argtypes = [C.c_char_p, C.POINTER(StackFileInfoC)]
+    L.cbb_reconstruct_file.restype = C.c_int
+    L.cbb_reconstruct_file.argtypes = [_VP, C.c_char_p, C.POINTER(OptionsC),
+                                       C.POINTER(RunStatsC)]
     L.cbb_compare_volumes_device.restype = C.c_int
     L.cbb_compare_volumes_device.argtypes = [_VP, _VP, C.c_int64, C.c_double,
                                              C.POINTER(VolumeDiffC), _VP]

@@ -148,6 +148,32 @@ def reconstruct_arrays(voxels: np.ndarray, geometry: VolumeGeometry, images: np.
     return st.to_dict()
 
 
+def stack_file_info(path: str) -> dict:
+    """Header of a CBPS stack file (cbb_stack_file_query); raises IOError_,
+    FormatError, TruncatedError like read_stack (proj/src/dataset.cpp:181-212)."""
+    info = _lib.StackFileInfoC()
+    _lib.check(_lib.lib().cbb_stack_file_query(str(path).encode(), C.byref(info)))
+    return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def reconstruct_file(path: str, options: Optional[Options] = None,
+                     initial: Optional[Volume] = None) -> tuple:
+    """Reconstructs a CBPS stack file, streaming its projections from disk
+    (cbb_reconstruct_file). Returns (Volume, run stats); `initial` (same
+    geometry) is accumulated into, like reconstruct()."""
+    info = stack_file_info(path)
+    g = VolumeGeometry(info["edge_voxels"], info["voxel_mm"], info["origin_mm"])
+    vol = Volume(g) if initial is None else initial
+    if vol.geometry != g:
+        from .errors import GeometryError
+        raise GeometryError("reconstruct_file: volume and stack geometries differ")
+    oc, _keep = (options or Options()).to_c()
+    st = _lib.RunStatsC()
+    _lib.check(_lib.lib().cbb_reconstruct_file(_ptr(vol.voxels), str(path).encode(),
+                                               C.byref(oc), C.byref(st)))
+    return vol, st.to_dict()
+
+
 class Session:
     """Streaming per-projection back-projection (cbb_session_*), the
     RabbitCT-style module interface: feed projections one by one, read the

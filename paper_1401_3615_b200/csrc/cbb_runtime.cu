@@ -27,6 +27,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include "../../include/conebeam_b200.h"
 #include "bp_kernels.cuh"
@@ -221,11 +224,12 @@ bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_beg
 
 constexpr int kR = 8; // voxels per thread along z
 
-void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaStream_t st) {
+void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaStream_t st,
+                 int* err = nullptr) {
     const int qp = quad_pitch_cells(W);
     const int qr = quad_rows(H);
     dim3 grid((qp + 127) / 128, qr, count);
-    pack_quads<<<grid, 128, 0, st>>>(raw, W, H, static_cast<float4*>(packed), qp, qr);
+    pack_quads<<<grid, 128, 0, st>>>(raw, W, H, static_cast<float4*>(packed), qp, qr, err);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -573,7 +577,7 @@ struct Pipeline {
             if (opt.ramp_filter)
                 ramp_filter_device(w->d_raw[slot], w->d_raw[slot], W, H, n, opt.filter_pixel_mm,
                                    w->compute);
-            launch_pack(w->d_raw[slot], W, H, n, w->d_packed[slot], w->compute);
+            launch_pack(w->d_raw[slot], W, H, n, w->d_packed[slot], w->compute, w->d_err);
             CK(cudaEventRecord(w->raw_free[slot], w->compute));
             w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end,
                                              w->d_packed[slot], W, H, n, mats, opt,
@@ -640,6 +644,55 @@ struct Pipeline {
         }
     }
 
+    // Streams the projection records of an open CBPS file (proj/src/dataset.cpp:
+    // 155-212 layout: per record 12 little-endian f64 then W*H f32) straight
+    // into the pinned staging slots: record i's image goes to its place in
+    // the batch, its matrix to a small host array. Reads of batch k+1 run on
+    // the host while the devices process batch k; each batch is read by a
+    // few threads with pread.
+    void submit_file(int fd, int count, uint64_t header_bytes, uint64_t rec_bytes) {
+        ensure_staging();
+        std::vector<double> mats(12 * (size_t)opt.batch);
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int nt = (int)std::min<unsigned>(8, hw);
+        for (int first = 0; first < count; first += opt.batch) {
+            const int n = std::min(opt.batch, count - first);
+            wait_slot(slot);
+            float* dst = h_stage[slot];
+            std::vector<std::thread> pool;
+            std::vector<int> bad(nt, 0);
+            for (int t = 0; t < nt; ++t)
+                pool.emplace_back([&, t] {
+                    for (int j = t; j < n; j += nt) {
+                        const uint64_t off = header_bytes + rec_bytes * (uint64_t)(first + j);
+                        if (!pread_all(fd, mats.data() + 12 * (size_t)j, 96, off) ||
+                            !pread_all(fd, dst + (size_t)j * W * H, rec_bytes - 96, off + 96))
+                            bad[t] = 1;
+                    }
+                });
+            for (auto& th : pool)
+                th.join();
+            for (int b : bad)
+                if (b)
+                    fail(CBB_ERR_TRUNCATED, "file ends inside projection intensities");
+            validate_matrices(mats.data(), n);
+            issue(dst, mats.data(), n);
+        }
+    }
+
+    static bool pread_all(int fd, void* buf, uint64_t bytes, uint64_t off) {
+        char* p = static_cast<char*>(buf);
+        while (bytes) {
+            const ssize_t r = ::pread(fd, p, bytes, (off_t)off);
+            if (r <= 0)
+                return false;
+            p += r;
+            off += (uint64_t)r;
+            bytes -= (uint64_t)r;
+        }
+        return true;
+    }
+
     // Waits for all work, checks the w == 0 flag, downloads slabs into vol_out.
     void finish(float* vol_out) {
         flush();
@@ -662,7 +715,9 @@ struct Pipeline {
             CK(cudaMemcpy(&e, w->d_err, sizeof(int), cudaMemcpyDeviceToHost));
             err_any |= e;
         }
-        if (err_any)
+        if (err_any & 2) // ProjectionImage::validate (proj/src/dataset.cpp:123-129)
+            fail(CBB_ERR_INVALID, "ProjectionImage contains non-finite values");
+        if (err_any & 1)
             fail(CBB_ERR_GEOMETRY, "backprojection hit a voxel with w == 0");
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
@@ -878,24 +933,75 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, cons
         Pipeline pipe;
         pipe.init(*geometry, width, height, opt, vol);
         pipe.submit_stack(imgs, mats, count);
-        // download into a private buffer first so a failure leaves vol intact
-        const size_t n = (size_t)geometry->edge_voxels * geometry->edge_voxels *
-                         geometry->edge_voxels;
-        if (opt.volume_is_zero) {
-            pipe.finish(vol);
-        } else {
-            std::vector<float> out(n);
-            pipe.finish(out.data());
-            const size_t plane = (size_t)geometry->edge_voxels * geometry->edge_voxels;
-            const int s0 = opt.slab_end ? opt.slab_begin : 0;
-            const int s1 = opt.slab_end ? opt.slab_end : geometry->edge_voxels;
-            std::memcpy(vol + plane * s0, out.data() + plane * s0,
-                        plane * (s1 - s0) * sizeof(float));
-        }
+        // finish() checks the error flags before any download, so on a
+        // geometry error vol is left unchanged; only the slab planes are written
+        pipe.finish(vol);
         const double total =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         pipe.fill_stats(stats, total);
     });
+}
+
+// CBPS header (proj/include/conebeam/dataset.hpp:62-72, proj/src/dataset.cpp:
+// 181-212): "CBPS", u16 version 1, u16 reserved, u32 W, u32 H, u32 count,
+// f64 voxel_mm, f64 origin_mm, u32 L; then count records of 96 + 4*W*H bytes.
+struct StackFile {
+    int fd = -1;
+    cbb_stack_file_info info{};
+    uint64_t header_bytes = 40, rec_bytes = 0;
+    ~StackFile() {
+        if (fd >= 0)
+            ::close(fd);
+    }
+};
+
+void open_stack_file(const char* path, StackFile& f) {
+    static_assert(sizeof(double) == 8 && sizeof(float) == 4, "IEEE sizes");
+    const uint16_t probe = 1;
+    if (*reinterpret_cast<const uint8_t*>(&probe) != 1)
+        fail(CBB_ERR_INTERNAL, "big-endian hosts are not supported by the streaming reader");
+    f.fd = ::open(path, O_RDONLY);
+    if (f.fd < 0)
+        fail(CBB_ERR_IO, "cannot open '%s' for reading", path);
+    unsigned char h[40];
+    if (!Pipeline::pread_all(f.fd, h, 4, 0))
+        fail(CBB_ERR_TRUNCATED, "file ends inside magic");
+    if (std::memcmp(h, "CBPS", 4) != 0)
+        fail(CBB_ERR_FORMAT, "not a stack file (magic mismatch)");
+    if (!Pipeline::pread_all(f.fd, h + 4, 4, 4))
+        fail(CBB_ERR_TRUNCATED, "file ends inside version");
+    uint16_t version;
+    std::memcpy(&version, h + 4, 2);
+    if (version != 1)
+        fail(CBB_ERR_FORMAT, "stack file version %u not supported (expected 1)", version);
+    if (!Pipeline::pread_all(f.fd, h + 8, 32, 8))
+        fail(CBB_ERR_TRUNCATED, "file ends inside header");
+    uint32_t W, H, N, L;
+    std::memcpy(&W, h + 8, 4);
+    std::memcpy(&H, h + 12, 4);
+    std::memcpy(&N, h + 16, 4);
+    std::memcpy(&f.info.voxel_mm, h + 20, 8);
+    std::memcpy(&f.info.origin_mm, h + 28, 8);
+    std::memcpy(&L, h + 36, 4);
+    if (W < 1 || H < 1 || N < 1)
+        fail(CBB_ERR_FORMAT, "stack header has zero width, height, or count");
+    if (W > (1u << 20) || H > (1u << 20) || N > (1u << 30) || L > (1u << 30))
+        fail(CBB_ERR_FORMAT, "stack header sizes out of range");
+    f.info.width = (int32_t)W;
+    f.info.height = (int32_t)H;
+    f.info.count = (int32_t)N;
+    f.info.edge_voxels = (int32_t)L;
+    const cbb_volume_geometry g{f.info.edge_voxels, f.info.voxel_mm, f.info.origin_mm};
+    validate_geometry(&g);
+    f.rec_bytes = 96 + 4ull * W * H;
+    struct stat st;
+    if (::fstat(f.fd, &st) != 0)
+        fail(CBB_ERR_IO, "cannot stat '%s'", path);
+    const uint64_t want = f.header_bytes + f.rec_bytes * N;
+    if ((uint64_t)st.st_size < want)
+        fail(CBB_ERR_TRUNCATED, "file ends inside projection intensities");
+    if ((uint64_t)st.st_size > want)
+        fail(CBB_ERR_FORMAT, "stack file has trailing bytes after payload");
 }
 
 cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry, const float* img,
@@ -905,6 +1011,37 @@ cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry, cons
     o.num_gpus = 1;
     o.batch = 1;
     return cbb_reconstruct(vol, geometry, img, width, height, 1, matrix12, &o, nullptr);
+}
+
+cbb_status cbb_stack_file_query(const char* path, cbb_stack_file_info* out) {
+    return guarded([&] {
+        if (!path || !out)
+            fail(CBB_ERR_INVALID, "cbb_stack_file_query: null argument");
+        StackFile f;
+        open_stack_file(path, f);
+        *out = f.info;
+    });
+}
+
+cbb_status cbb_reconstruct_file(float* vol, const char* path, const cbb_options* options,
+                                cbb_run_stats* stats) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!vol || !path)
+            fail(CBB_ERR_INVALID, "cbb_reconstruct_file: null argument");
+        StackFile f;
+        open_stack_file(path, f);
+        validate_detector(f.info.width, f.info.height);
+        const cbb_options opt = resolve_options(options);
+        const cbb_volume_geometry g{f.info.edge_voxels, f.info.voxel_mm, f.info.origin_mm};
+        Pipeline pipe;
+        pipe.init(g, f.info.width, f.info.height, opt, vol);
+        pipe.submit_file(f.fd, f.info.count, f.header_bytes, f.rec_bytes);
+        pipe.finish(vol);
+        const double total =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        pipe.fill_stats(stats, total);
+    });
 }
 
 cbb_status cbb_session_create(const cbb_volume_geometry* geometry, int32_t width,

@@ -155,6 +155,29 @@ def test_distributed_driver_single_rank(cuda):
     assert bits_equal(rec.gather(slab), expected)
 
 
+def test_reconstruct_file_streaming(cuda, tmp_path):
+    """CBPS file -> cbb_reconstruct_file (streamed from disk, batch 4) is
+    bitwise the reference fixture; a NaN pixel is rejected like
+    ProjectionStack::validate (proj/src/dataset.cpp:123-144)."""
+    g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
+    p = str(tmp_path / "mini.cbps")
+    pkg.write_stack(p, pkg.ProjectionStack(g, mats, imgs))
+    vol, st = pkg.reconstruct_file(p, pkg.Options(batch=4), initial=pkg.Volume(g, vol0.copy()))
+    assert bits_equal(vol.voxels, expected)
+    assert st["voxel_updates"] == g.edge_voxels ** 3 * len(mats)
+    bad = imgs.copy()
+    bad[3, 5, 7] = np.nan
+    raw = bytearray(open(p, "rb").read())
+    off = 40 + 3 * (96 + 4 * imgs.shape[1] * imgs.shape[2]) + 96 + 4 * (5 * imgs.shape[2] + 7)
+    raw[off:off + 4] = np.float32(np.nan).tobytes()
+    open(p, "wb").write(bytes(raw))
+    keep = vol0.copy()
+    v2 = pkg.Volume(g, vol0.copy())
+    with pytest.raises(pkg.ValidationError):
+        pkg.reconstruct_file(p, initial=v2)
+    assert bits_equal(v2.voxels, keep)
+
+
 def test_fast_mode_within_tolerance(cuda):
     g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
     v, _ = gpu_reconstruct(g, mats, imgs, vol0, mode=pkg.MODE_FAST)

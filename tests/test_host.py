@@ -191,3 +191,31 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.VolumeGeometryC) == 24
     assert ctypes.sizeof(_lib.OptionsC) == 56
     assert ctypes.sizeof(_lib.RunStatsC) == 8 * 4 + 8 * 2 + 8 + 8 * 8
+    assert ctypes.sizeof(_lib.StackFileInfoC) == 40
+
+
+# --- CBPS header through the C ABI (host-only code path) -------------------------
+
+def test_stack_file_query_matches_reader(tmp_path):
+    s = two_image_stack()
+    p = str(tmp_path / "q.cbps")
+    pkg.write_stack(p, s)
+    info = pkg.stack_file_info(p)
+    assert info == {"edge_voxels": 4, "voxel_mm": 1.0, "origin_mm": -1.5, "count": 2,
+                    "width": 4, "height": 3}
+
+
+def test_stack_file_query_error_mapping(tmp_path):
+    # same exception classes as read_stack (proj/tests/test_dataset.cpp:76-128)
+    p = str(tmp_path / "e.cbps")
+    pkg.write_stack(p, two_image_stack())
+    raw = bytearray(open(p, "rb").read())
+    cases = [(b"SPBC" + raw[4:], pkg.FormatError), (raw[:4] + b"\x09" + raw[5:], pkg.FormatError),
+             (raw[:-7], pkg.TruncatedError), (raw + b"\0", pkg.FormatError),
+             (raw[:20], pkg.TruncatedError)]
+    for data, exc in cases:
+        open(p, "wb").write(bytes(data))
+        with pytest.raises(exc):
+            pkg.stack_file_info(p)
+    with pytest.raises(pkg.IOError_):
+        pkg.stack_file_info(str(tmp_path / "missing.cbps"))
