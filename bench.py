@@ -424,6 +424,28 @@ def run_ours(args):
                 sl3 = (0, g3.edge_voxels)
             sec.append(dict(workload=synth.CONFIGS[3].name, mode=args.mode,
                             **measure(g3, mode, 3, sl3)))
+        # north_star's hardware-texture side number (not parity-exact)
+        from paper_1401_3615_b200.backproject import backproject_texture_device
+        vt = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+
+        def st_tex():
+            vt.zero_()
+            backproject_texture_device(vt, g, z0, z1, imgs, mats, stream)
+        st_tex()
+        torch.cuda.synchronize()
+        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ta.record(stream)
+        for _ in range(3):
+            st_tex()
+        tb.record(stream)
+        torch.cuda.synchronize()
+        ms_t = ta.elapsed_time(tb) / 3
+        dtex = pkg.compare_volumes_device(vt, vol)  # vs this run's main-mode volume
+        sec.append({"workload": cfg.name, "mode": "texture (side number, not parity-exact)",
+                    "value": round(L ** 3 * n / (ms_t * 1e-3) / 1e9, 3), "unit": "GUp/s",
+                    "ms_per_step": round(ms_t, 3),
+                    "vs_" + args.mode: {k: dtex[k] for k in ("rel_l2", "max_abs_over_range")}})
+        del vt
         line["secondary"] = sec
         torch.cuda.empty_cache()
 

@@ -193,6 +193,16 @@ cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* ge
 cbb_status cbb_ramp_filter_device(const float* raw, float* out, int32_t width, int32_t height,
                                   int32_t count, double pixel_mm, void* stream);
 
+/* Side variant (north_star: "reported separately, only as a side number"):
+ * hardware-texture bilinear back-projection of raw (unpacked) projections,
+ * FMA coordinates and an approximate reciprocal. It does NOT match the
+ * reference (8-bit texture weights, floor addressing); see DESIGN.md for its
+ * measured deviation. Synchronous per batch of 32. */
+cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                          int32_t z_begin, int32_t z_end, const float* raw,
+                                          int32_t width, int32_t height, int32_t count,
+                                          const double* mats, void* stream);
+
 /* Volume comparison on the device: quality_metrics (proj/src/bench.cpp:65-82),
  * max_relative_error (:92-102) and the north_star parity figures. */
 typedef struct cbb_volume_diff {

@@ -22,6 +22,7 @@ EXPORTS = (
     "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
     "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
     "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
+    "cbb_backproject_texture_device",
 )
 
 
@@ -113,6 +114,10 @@ def _declare(L) -> None:
     L.cbb_ramp_filter_device.restype = C.c_int
     L.cbb_ramp_filter_device.argtypes = [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                          _VP]
+    L.cbb_backproject_texture_device.restype = C.c_int
+    L.cbb_backproject_texture_device.argtypes = [_VP, C.POINTER(VolumeGeometryC), C.c_int32,
+                                                 C.c_int32, _VP, C.c_int32, C.c_int32,
+                                                 C.c_int32, _VP, _VP]
     L.cbb_stack_file_query.restype = C.c_int
     L.cbb_stack_file_query.argtypes = [C.c_char_p, C.POINTER(StackFileInfoC)]
     L.cbb_reconstruct_file.restype = C.c_int

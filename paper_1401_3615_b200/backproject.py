@@ -320,6 +320,24 @@ def compare_volumes_device(test, ref, denom_floor: float = 1e-6, stream=None) ->
     return out.to_dict()
 
 
+def backproject_texture_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: int,
+                               raw, matrices: np.ndarray, stream=None) -> None:
+    """Side variant: hardware-texture bilinear back-projection of raw CUDA
+    float32 projections (N, H, W) -- NOT parity-exact (8-bit texture weights,
+    floor addressing, FMA coordinates); reported only as a side number."""
+    import torch
+
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
+        raise ValidationError("backproject_texture_device: raw must be CUDA float32 (N, H, W)")
+    m = validate_matrices(matrices)
+    n, h, w = raw.shape
+    g = geometry_c(geometry)
+    s = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    _lib.check(_lib.lib().cbb_backproject_texture_device(
+        vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end), raw.data_ptr(), w, h, n,
+        _ptr(m), C.c_void_p(s.cuda_stream)))
+
+
 def launch_count() -> int:
     return int(_lib.lib().cbb_launch_count())
 

@@ -35,6 +35,7 @@
 #include "bp_kernels.cuh"
 #include "ramp_filter.cuh"
 #include "metrics.cuh"
+#include "texture_variant.cuh"
 
 namespace cbb {
 
@@ -865,6 +866,70 @@ cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64
         out->ref_max = rmax;
         out->max_abs_over_range = rmax > rmin ? mabs / (rmax - rmin) : (mabs > 0 ? INFINITY : 0.0);
         out->bitwise_different = nd;
+    });
+}
+
+cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                          int32_t z_begin, int32_t z_end, const float* raw,
+                                          int32_t width, int32_t height, int32_t count,
+                                          const double* mats, void* stream) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        if (!vol_slab || !raw || !mats)
+            fail(CBB_ERR_INVALID, "cbb_backproject_texture_device: null argument");
+        if (width < 1 || height < 1 || count < 1)
+            fail(CBB_ERR_INVALID, "cbb_backproject_texture_device: empty input");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin >= z_end)
+            fail(CBB_ERR_INVALID, "cbb_backproject_texture_device: bad slab");
+        validate_matrices(mats, count);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int L = geometry->edge_voxels;
+        constexpr int kLayers = 2048; // layered-texture depth limit
+        for (int chunk0 = 0; chunk0 < count; chunk0 += kLayers) {
+            const int nc = std::min(kLayers, count - chunk0);
+            cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
+            cudaArray_t arr = nullptr;
+            CK(cudaMalloc3DArray(&arr, &fd, make_cudaExtent(width, height, nc), cudaArrayLayered));
+            cudaMemcpy3DParms cp = {};
+            cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(raw) + (size_t)chunk0 * width * height,
+                                            (size_t)width * sizeof(float), width, height);
+            cp.dstArray = arr;
+            cp.extent = make_cudaExtent(width, height, nc);
+            cp.kind = cudaMemcpyDeviceToDevice;
+            cudaError_t e = cudaMemcpy3DAsync(&cp, st);
+            cudaResourceDesc rd = {};
+            rd.resType = cudaResourceTypeArray;
+            rd.res.array.array = arr;
+            cudaTextureDesc td = {};
+            td.addressMode[0] = td.addressMode[1] = cudaAddressModeBorder;
+            td.filterMode = cudaFilterModeLinear;
+            td.readMode = cudaReadModeElementType;
+            td.normalizedCoords = 0;
+            cudaTextureObject_t tex = 0;
+            if (e == cudaSuccess)
+                e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+            for (int first = 0; e == cudaSuccess && first < nc; first += kMaxBatch) {
+                const int n = std::min(kMaxBatch, nc - first);
+                BpMats m;
+                for (int p = 0; p < n; ++p)
+                    store_matrix(m.a[p], mats + 12 * (size_t)(chunk0 + first + p));
+                constexpr int R = 8;
+                dim3 grid((L + kBlockX - 1) / kBlockX, (L + kBlockY - 1) / kBlockY,
+                          (z_end - z_begin + R - 1) / R);
+                bp_texture_kernel<R><<<grid, 256, 0, st>>>(
+                    vol_slab, L, z_begin, z_end, (float)geometry->origin_mm,
+                    (float)geometry->voxel_mm, tex, first, n, m);
+                ++g_launches;
+                e = cudaGetLastError();
+            }
+            // the array and texture are released once the chunk has run
+            const cudaError_t es = cudaStreamSynchronize(st);
+            if (tex)
+                cudaDestroyTextureObject(tex);
+            cudaFreeArray(arr);
+            CK(e);
+            CK(es);
+        }
     });
 }
 
