@@ -240,7 +240,7 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
     args.nby = (args.L + kBlockY - 1) / kBlockY;
-    args.nbz = (nz + R - 1) / R;
+    args.nbz = (nz - args.gap + R - 1) / R;
     dim3 block(kBlockX * kBlockY);
     dim3 grid(args.nbx, args.nby, args.nbz);
     if (SW) {
@@ -278,7 +278,7 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
 uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z_begin,
                             int z_end, const void* packed, int W, int H, int count,
                             const double* mats, const cbb_options& opt, int* err,
-                            cudaStream_t st) {
+                            cudaStream_t st, int gap_lo = 0, int gap_hi = 0) {
     const int qp = quad_pitch_cells(W);
     const int qr = quad_rows(H);
     const long long proj_bytes = (long long)qp * qr * 16;
@@ -297,6 +297,10 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.err = err;
     args.neg_zero2 = 0x8000000080000000ull;
     args.cull = opt.cull ? 1 : 0;
+    // optional skipped planes [gap_lo, gap_hi) (absolute z, gap_lo - z_begin
+    // a multiple of 8 so that every z-block stays on one side of the gap)
+    args.gap_at = gap_hi > gap_lo ? gap_lo - z_begin : (1 << 30);
+    args.gap = gap_hi > gap_lo ? gap_hi - gap_lo : 0;
     uint64_t guarded_launches = 0;
     const int nz = z_end - z_begin;
     if (nz <= 0 || count <= 0)
@@ -349,19 +353,25 @@ class DevicePool {
         return p;
     }
 
+    // A cached block for the request, or nullptr (never allocates).
+    void* take_cached(int device, size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        std::lock_guard<std::mutex> lk(mu_);
+        auto& fl = free_[device];
+        auto it = fl.lower_bound(bytes);
+        if (it != fl.end() && it->first <= 2 * bytes) {
+            void* p = it->second;
+            sizes_[p] = it->first;
+            fl.erase(it);
+            return p;
+        }
+        return nullptr;
+    }
+
     void* alloc(int device, size_t bytes) {
         bytes = std::max<size_t>(bytes, 256);
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            auto& fl = free_[device];
-            auto it = fl.lower_bound(bytes);
-            if (it != fl.end() && it->first <= 2 * bytes) {
-                void* p = it->second;
-                sizes_[p] = it->first;
-                fl.erase(it);
-                return p;
-            }
-        }
+        if (void* c = take_cached(device, bytes))
+            return c;
         void* p = nullptr;
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e == cudaErrorMemoryAllocation) {
@@ -416,6 +426,13 @@ struct Worker {
     double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
     uint64_t guarded = 0;
     bool started = false;
+    // resident mode: every packed projection stays on the device; the head
+    // planes [z_begin, tail_lo) + [tail_hi, z_end) are updated while the
+    // batches stream in, the tail [tail_lo, tail_hi) afterwards while the
+    // head is copied back
+    void* d_packed_all = nullptr;
+    int tail_lo = 0, tail_hi = 0;
+    cudaEvent_t head_done = nullptr, tail_done = nullptr;
 
     ~Worker() {
         if (!copy)
@@ -432,6 +449,11 @@ struct Worker {
             cudaEventDestroy(raw_free[i]);
         }
         pool.release(device, d_err);
+        pool.release(device, d_packed_all);
+        if (head_done)
+            cudaEventDestroy(head_done);
+        if (tail_done)
+            cudaEventDestroy(tail_done);
         cudaEventDestroy(k_beg);
         cudaEventDestroy(k_end);
         cudaEventDestroy(c_beg);
@@ -484,6 +506,120 @@ struct Pipeline {
     uint64_t submitted = 0;
     size_t raw_bytes_per_proj = 0;
     size_t packed_bytes_per_proj = 0;
+    bool resident = false;         // see Worker::d_packed_all
+    int resident_count = 0;
+    std::vector<double> all_mats;  // resident mode: every matrix, for the tail pass
+    const double* est_mats = nullptr; // matrices for choose_tails (else the first batch)
+    int est_n = 0;
+
+    // Resident mode for a stack of known size: when every packed projection
+    // fits in device memory (with 2 GB to spare), keep them all so a dense
+    // tail of each slab (choose_tails) can be back-projected after the stream
+    // ends while the rest is already copied to the host (hides most of the
+    // D2H).
+    void enable_resident(int count) {
+        if (std::getenv("CBB_NO_RESIDENT"))
+            return;
+        const size_t need = packed_bytes_per_proj * (size_t)count;
+        for (auto& w : workers)
+            if (w->z_end - w->z_begin < 16)
+                return;
+        std::vector<void*> blocks;
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            void* p = DevicePool::get().take_cached(w->device, need);
+            if (!p) {
+                size_t free_b = 0, total_b = 0;
+                CK(cudaMemGetInfo(&free_b, &total_b));
+                if (free_b >= need + (size_t(2) << 30))
+                    p = DevicePool::get().alloc(w->device, need);
+                else if (std::getenv("CBB_TRACE"))
+                    std::fprintf(stderr, "cbb: resident off, need %zu free %zu\n", need, free_b);
+            }
+            if (!p) {
+                for (size_t i = 0; i < blocks.size(); ++i)
+                    DevicePool::get().release(workers[i]->device, blocks[i]);
+                return;
+            }
+            blocks.push_back(p);
+        }
+        for (size_t i = 0; i < workers.size(); ++i) {
+            auto& w = workers[i];
+            CK(cudaSetDevice(w->device));
+            w->d_packed_all = blocks[i];
+            if (!w->head_done) {
+                CK(cudaEventCreate(&w->head_done));
+                CK(cudaEventCreateWithFlags(&w->tail_done, cudaEventDisableTiming));
+            }
+        }
+        resident = true;
+        resident_count = count;
+        all_mats.assign(12 * (size_t)count, 0.0);
+    }
+
+    // Picks each worker's tail: the contiguous run of 8-plane groups with the
+    // fewest planes that holds ~kTailFrac of the slab's estimated work. Work
+    // per group = fraction of sampled (x, y, projection) positions that land
+    // on the detector (the rest is culled warp by warp) + a fixed overhead,
+    // sampled on a 16 x 16 grid at the group's centre plane for up to 8 of
+    // the given projections. A dense tail keeps its D2H short while its
+    // compute hides the head's D2H.
+    void choose_tails(const double* mats, int n) {
+        double frac = 0.12;
+        if (const char* e = std::getenv("CBB_TAIL_FRAC"))
+            frac = std::atof(e);
+        const int L = g.edge_voxels, S = 16, NP = std::min(n, 8);
+        for (auto& w : workers) {
+            std::vector<double> gw;
+            std::vector<int> gz;
+            for (int z = w->z_begin; z < w->z_end; z += 8) {
+                const int pz = std::min(8, w->z_end - z);
+                const double zc = g.origin_mm + (z + (pz - 1) * 0.5) * g.voxel_mm;
+                int on = 0;
+                for (int k = 0; k < NP; ++k) {
+                    const double* a = mats + 12 * (size_t)((long long)k * n / NP);
+                    for (int j = 0; j < S; ++j)
+                        for (int i = 0; i < S; ++i) {
+                            const double x = g.origin_mm + (L - 1) * (i / (S - 1.0)) * g.voxel_mm;
+                            const double y = g.origin_mm + (L - 1) * (j / (S - 1.0)) * g.voxel_mm;
+                            const double u = a[0] * x + a[3] * y + a[6] * zc + a[9];
+                            const double v = a[1] * x + a[4] * y + a[7] * zc + a[10];
+                            const double ww = a[2] * x + a[5] * y + a[8] * zc + a[11];
+                            const double ix = u / ww, iy = v / ww;
+                            on += ix > -2 && ix < W && iy > -2 && iy < H;
+                        }
+                }
+                gw.push_back(pz * ((double)on / (NP * S * S) + 0.05));
+                gz.push_back(z);
+            }
+            gz.push_back(w->z_end);
+            const int G = (int)gw.size();
+            double total = 0.0;
+            for (double x : gw)
+                total += x;
+            int best_i = G - 1, best_j = G, best_planes = 1 << 30;
+            for (int i = 0; i < G; ++i) {
+                double s = 0.0;
+                for (int j = i; j < G; ++j) {
+                    s += gw[j];
+                    if (s >= frac * total) {
+                        const int planes = gz[j + 1] - gz[i];
+                        if (planes < best_planes && !(i == 0 && j == G - 1)) {
+                            best_planes = planes;
+                            best_i = i;
+                            best_j = j + 1;
+                        }
+                        break;
+                    }
+                }
+            }
+            w->tail_lo = gz[best_i];
+            w->tail_hi = gz[best_j];
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: device %d slab [%d, %d) tail [%d, %d)\n", w->device,
+                             w->z_begin, w->z_end, w->tail_lo, w->tail_hi);
+        }
+    }
 
     ~Pipeline() {
         workers.clear();
@@ -564,6 +700,14 @@ struct Pipeline {
     // corresponding h2d_done events complete (wait_slot).
     void issue(const float* src, const double* mats, int n) {
         const size_t bytes = raw_bytes_per_proj * n;
+        if (resident && submitted == 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: choose_tails %.2f ms\n",
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
+        }
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             // raw[slot] may still be read by the pack of batch (k-2)
@@ -578,14 +722,34 @@ struct Pipeline {
             if (opt.ramp_filter)
                 ramp_filter_device(w->d_raw[slot], w->d_raw[slot], W, H, n, opt.filter_pixel_mm,
                                    w->compute);
-            launch_pack(w->d_raw[slot], W, H, n, w->d_packed[slot], w->compute, w->d_err);
+            void* packed = resident ? static_cast<char*>(w->d_packed_all) +
+                                          packed_bytes_per_proj * submitted
+                                    : w->d_packed[slot];
+            launch_pack(w->d_raw[slot], W, H, n, packed, w->compute, w->d_err);
             CK(cudaEventRecord(w->raw_free[slot], w->compute));
-            w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end,
-                                             w->d_packed[slot], W, H, n, mats, opt,
-                                             w->d_err, w->compute);
+            // resident: the head, i.e. the slab minus the tail planes
+            w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end, packed, W, H, n,
+                                             mats, opt, w->d_err, w->compute,
+                                             resident ? w->tail_lo : 0, resident ? w->tail_hi : 0);
         }
+        if (resident)
+            std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
         submitted += n;
         slot ^= 1;
+    }
+
+    // Host-side proof that every batch of the tail pass runs unguarded (no
+    // possible w == 0 error), so the head may be copied out before the tail
+    // is computed.
+    bool tail_is_safe(const Worker& w) const {
+        const float Of = (float)g.origin_mm, MMf = (float)g.voxel_mm;
+        const double cxy = min_nonzero_coord(Of, MMf, 0, g.edge_voxels);
+        const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, w.tail_lo, w.tail_hi)};
+        for (int p = 0; p < resident_count; ++p)
+            if (!projection_is_safe(all_mats.data() + 12 * (size_t)p, g, w.tail_lo, w.tail_hi,
+                                    cmin))
+                return false;
+        return true;
     }
 
     // Blocks until no device still reads the staging slot s.
@@ -621,18 +785,37 @@ struct Pipeline {
         stage_fill = 0;
     }
 
+    // Size of the batch starting at projection `first` of a stream: 4, 4, 8,
+    // 16, ... up to opt.batch, so the first back-projection starts after a
+    // small upload instead of a full batch (pipeline fill). Batch boundaries
+    // do not change any result: each voxel still accumulates the projections
+    // one by one in stack order.
+    int batch_at(int first, int count) const {
+        return std::min({opt.batch, std::max(4, first), count - first});
+    }
+
     // Whole-stack submission straight from the caller's buffer: pinned
     // buffers are copied asynchronously in place, pageable ones are staged
     // through the pinned double buffer.
     void submit_stack(const float* imgs, const double* mats, int count) {
+        if (submitted == 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            enable_resident(count);
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
+            est_mats = mats;
+            est_n = count;
+        }
         cudaPointerAttributes attr;
         bool pinned = false;
         if (cudaPointerGetAttributes(&attr, imgs) == cudaSuccess)
             pinned = attr.type == cudaMemoryTypeHost;
         else
             cudaGetLastError();
-        for (int first = 0; first < count; first += opt.batch) {
-            const int n = std::min(opt.batch, count - first);
+        for (int first = 0, n = 0; first < count; first += n) {
+            n = batch_at(first, count);
             const float* src = imgs + (size_t)first * W * H;
             if (pinned) {
                 issue(src, mats + 12 * (size_t)first, n);
@@ -652,12 +835,14 @@ struct Pipeline {
     // the host while the devices process batch k; each batch is read by a
     // few threads with pread.
     void submit_file(int fd, int count, uint64_t header_bytes, uint64_t rec_bytes) {
+        if (submitted == 0)
+            enable_resident(count);
         ensure_staging();
         std::vector<double> mats(12 * (size_t)opt.batch);
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const int nt = (int)std::min<unsigned>(8, hw);
-        for (int first = 0; first < count; first += opt.batch) {
-            const int n = std::min(opt.batch, count - first);
+        for (int first = 0, n = 0; first < count; first += n) {
+            n = batch_at(first, count);
             wait_slot(slot);
             float* dst = h_stage[slot];
             std::vector<std::thread> pool;
@@ -695,20 +880,16 @@ struct Pipeline {
     }
 
     // Waits for all work, checks the w == 0 flag, downloads slabs into vol_out.
-    void finish(float* vol_out) {
-        flush();
-        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
-        for (auto& w : workers) {
-            CK(cudaSetDevice(w->device));
-            if (w->started) {
-                CK(cudaEventRecord(w->k_end, w->compute));
-            }
-        }
+    // Synchronizes every worker's compute stream and raises the first error
+    // the kernels flagged (nothing has been written to the host yet).
+    void check_errors(bool close_timing) {
         int err_any = 0;
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
+            if (close_timing && w->started)
+                CK(cudaEventRecord(w->k_end, w->compute));
             CK(cudaStreamSynchronize(w->compute));
-            if (w->started) {
+            if (close_timing && w->started) {
                 w->kernel_s += elapsed_s(w->k_beg, w->k_end);
                 w->started = false;
             }
@@ -720,6 +901,17 @@ struct Pipeline {
             fail(CBB_ERR_INVALID, "ProjectionImage contains non-finite values");
         if (err_any & 1)
             fail(CBB_ERR_GEOMETRY, "backprojection hit a voxel with w == 0");
+    }
+
+    // Waits for all work, checks the error flags, downloads slabs into vol_out.
+    void finish(float* vol_out) {
+        flush();
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        if (resident) {
+            finish_resident(vol_out);
+            return;
+        }
+        check_errors(true);
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             const size_t slab = plane * (w->z_end - w->z_begin);
@@ -733,6 +925,82 @@ struct Pipeline {
             CK(cudaEventSynchronize(w->c_end));
             w->d2h_s += elapsed_s(w->c_beg, w->c_end);
         }
+    }
+
+    // Resident mode: the head planes are complete once the stream has been
+    // consumed; the tail planes are back-projected from the resident packed
+    // projections while the head is copied to the host (copy stream). The
+    // head is released early only when no tail batch can raise an error
+    // (tail_is_safe, no guarded head batch); otherwise everything is checked
+    // before any byte reaches vol_out.
+    void finish_resident(float* vol_out) {
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        check_errors(false);
+        bool overlap = true;
+        for (auto& w : workers)
+            overlap = overlap && w->guarded == 0 && tail_is_safe(*w);
+        const bool trace = std::getenv("CBB_TRACE") != nullptr;
+        cudaEvent_t t_tail = nullptr;
+        auto d2h = [&](Worker& w, int z0, int z1) {
+            if (z1 > z0)
+                CK(cudaMemcpyAsync(vol_out + plane * z0, w.d_vol + plane * (z0 - w.z_begin),
+                                   plane * (z1 - z0) * sizeof(float), cudaMemcpyDeviceToHost,
+                                   w.copy));
+        };
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (trace && w == workers.front()) {
+                CK(cudaEventCreate(&t_tail));
+                CK(cudaEventRecord(t_tail, w->compute));
+            }
+            if (!overlap) {
+                w->guarded += launch_backproject(
+                    w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
+                    w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
+                    w->compute);
+                continue;
+            }
+            // head out now; the tail copied out as soon as it is computed (no
+            // error can arise in it: tail_is_safe)
+            CK(cudaEventRecord(w->c_beg, w->copy));
+            d2h(*w, w->z_begin, w->tail_lo);
+            d2h(*w, w->tail_hi, w->z_end);
+            CK(cudaEventRecord(w->head_done, w->copy));
+            launch_backproject(w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo,
+                               w->tail_hi, w->d_packed_all, W, H, resident_count,
+                               all_mats.data(), opt, w->d_err, w->compute);
+            CK(cudaEventRecord(w->tail_done, w->compute));
+            CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
+            d2h(*w, w->tail_lo, w->tail_hi);
+            CK(cudaEventRecord(w->c_end, w->copy));
+        }
+        // closes the kernel timing; with overlap this only re-checks flags
+        // that cannot be set (pack errors were checked above)
+        check_errors(true);
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (!overlap) {
+                CK(cudaEventRecord(w->c_beg, w->copy));
+                d2h(*w, w->z_begin, w->z_end);
+                CK(cudaEventRecord(w->c_end, w->copy));
+            }
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->d2h_s += elapsed_s(w->c_beg, w->c_end);
+        }
+        if (t_tail) {
+            auto& w = *workers.front();
+            std::fprintf(stderr,
+                         "cbb: resident, overlap %d, tail [%d, %d): k_beg->tail %.2f ms, "
+                         "head d2h %.2f ms, k_beg->k_end %.2f ms, k_beg->c_end %.2f ms\n",
+                         (int)overlap, w.tail_lo, w.tail_hi, elapsed_s(w.k_beg, t_tail) * 1e3,
+                         overlap ? elapsed_s(w.c_beg, w.head_done) * 1e3 : 0.0,
+                         elapsed_s(w.k_beg, w.k_end) * 1e3, elapsed_s(w.k_beg, w.c_end) * 1e3);
+            cudaEventDestroy(t_tail);
+        }
+        resident = false;
     }
 
     void fill_stats(cbb_run_stats* st, double total) const {
@@ -995,15 +1263,31 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, cons
             fail(CBB_ERR_INVALID, "ProjectionStack: at least one projection required");
         validate_matrices(mats, count);
         const cbb_options opt = resolve_options(options);
-        Pipeline pipe;
-        pipe.init(*geometry, width, height, opt, vol);
-        pipe.submit_stack(imgs, mats, count);
-        // finish() checks the error flags before any download, so on a
-        // geometry error vol is left unchanged; only the slab planes are written
-        pipe.finish(vol);
+        const bool trace = std::getenv("CBB_TRACE") != nullptr;
+        auto ms = [&] {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                .count();
+        };
+        double t_init = 0, t_sub = 0, t_fin = 0;
+        {
+            Pipeline pipe;
+            pipe.init(*geometry, width, height, opt, vol);
+            t_init = ms();
+            pipe.submit_stack(imgs, mats, count);
+            t_sub = ms();
+            // finish() checks the error flags before any download, so on a
+            // geometry error vol is left unchanged; only the slab planes are written
+            pipe.finish(vol);
+            t_fin = ms();
+            pipe.fill_stats(stats, 0.0);
+        }
         const double total =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        pipe.fill_stats(stats, total);
+        if (stats)
+            stats->total_seconds = total;
+        if (trace)
+            std::fprintf(stderr, "cbb: host init %.2f submit %.2f finish %.2f teardown %.2f ms\n",
+                         t_init, t_sub, t_fin, total * 1e3);
     });
 }
 

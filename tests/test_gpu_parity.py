@@ -202,6 +202,47 @@ def test_reconstruct_file_streaming(cuda, tmp_path):
     assert bits_equal(v2.voxels, keep)
 
 
+@pytest.mark.parametrize("ids", [[0], [0, 0]])
+def test_resident_tail_overlap_bitwise(cuda, oracle, monkeypatch, ids):
+    """cbb_reconstruct keeps every packed projection resident and computes a
+    dense tail of each slab after the stream (overlapping the head's D2H):
+    bitwise the same as the streaming-only pipeline (CBB_NO_RESIDENT) and the
+    oracle, with one and two slab workers, ragged batches."""
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=70)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=35)
+    imgs = imgs_t.numpy()
+    ref = np.zeros((64,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    monkeypatch.setenv("CBB_NO_RESIDENT", "1")
+    plain, _ = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=16)
+    monkeypatch.delenv("CBB_NO_RESIDENT")
+    for frac in ("0.05", "0.12", "0.5"):
+        monkeypatch.setenv("CBB_TAIL_FRAC", frac)
+        v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=16)
+        assert st["guarded_batches"] == 0
+        assert bits_equal(v, plain)
+        assert bits_equal(v, ref)
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_w_zero_inside_slab_leaves_volume(cuda, monkeypatch, resident):
+    """w == 0 exactly on plane z = 20 of a 32^3 volume (w = world z): the
+    guarded kernel flags it and cbb_reconstruct raises GeometryError before
+    writing any plane, whether or not the resident tail pass is used."""
+    if not resident:
+        monkeypatch.setenv("CBB_NO_RESIDENT", "1")
+    g = VolumeGeometry(32, 1.0, -20.0)
+    m = np.zeros((3, 12))
+    m[:, 0] = m[:, 4] = 1.0
+    m[:, 8] = 1.0
+    m[:, 9] = m[:, 10] = 4.0
+    imgs = np.ones((3, 16, 16), np.float32)
+    vol = pkg.Volume(g, np.full((32, 32, 32), 3.0, np.float32))
+    with pytest.raises(pkg.GeometryError):
+        pkg.reconstruct(vol, pkg.ProjectionStack(g, m, imgs))
+    assert np.all(vol.voxels == 3.0)
+
+
 def test_fast_mode_within_tolerance(cuda):
     g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
     v, _ = gpu_reconstruct(g, mats, imgs, vol0, mode=pkg.MODE_FAST)
