@@ -225,12 +225,41 @@ bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_beg
 
 constexpr int kR = 8; // voxels per thread along z
 
+// Detector rows a worker holds and packed cell rows it packs (see
+// pack_quads). full(): the whole detector.
+struct RowBand {
+    int r0 = 0, rn = 0; // raw rows [r0, r0 + rn)
+    int q0 = 0, qn = 0; // packed rows [q0, q0 + qn), packed row = py + kPad
+    static RowBand full(int H) { return RowBand{0, H, 0, quad_rows(H)}; }
+    bool is_full(int H) const { return r0 == 0 && rn == H && q0 == 0 && qn == quad_rows(H); }
+};
+
+// Packs `count` projections whose raw rows [band.r0, band.r0 + band.rn) lie
+// raw_stride floats apart (band.rn * W for a band buffer, W * H for a full one
+// with raw pointing at row 0 -- then pass raw_row0 = 0, raw_rows = H).
+void launch_pack_band(const float* raw, int raw_row0, int raw_rows, long long raw_stride, int W,
+                      int H, int count, void* packed, const RowBand& band, cudaStream_t st,
+                      int* err) {
+    const int qp = quad_pitch_cells(W);
+    dim3 grid((qp + 127) / 128, band.qn, count);
+    if (band.qn <= 0 || count <= 0)
+        return;
+    pack_quads<<<grid, 128, 0, st>>>(raw, W, H, raw_row0, raw_rows, raw_stride,
+                                     static_cast<float4*>(packed), qp, band.q0, band.qn, err);
+    CK(cudaGetLastError());
+    ++g_launches;
+}
+
 void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaStream_t st,
                  int* err = nullptr) {
-    const int qp = quad_pitch_cells(W);
-    const int qr = quad_rows(H);
-    dim3 grid((qp + 127) / 128, qr, count);
-    pack_quads<<<grid, 128, 0, st>>>(raw, W, H, static_cast<float4*>(packed), qp, qr, err);
+    launch_pack_band(raw, 0, H, (long long)W * H, W, H, count, packed, RowBand::full(H), st, err);
+}
+
+void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st) {
+    if (n <= 0)
+        return;
+    const long long blocks = std::min<long long>(148 * 4, (n / 4 + 255) / 256 + 1);
+    check_finite<<<(unsigned)blocks, 256, 0, st>>>(v, n, err);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -278,10 +307,13 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
 uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z_begin,
                             int z_end, const void* packed, int W, int H, int count,
                             const double* mats, const cbb_options& opt, int* err,
-                            cudaStream_t st, int gap_lo = 0, int gap_hi = 0) {
+                            cudaStream_t st, int gap_lo = 0, int gap_hi = 0,
+                            const RowBand* band = nullptr) {
     const int qp = quad_pitch_cells(W);
-    const int qr = quad_rows(H);
-    const long long proj_bytes = (long long)qp * qr * 16;
+    const RowBand b = band ? *band : RowBand::full(H);
+    // packed projections of qn rows each; cell row q0 is the buffer's first
+    const long long proj_bytes = (long long)qp * b.qn * 16;
+    const long long band_shift = (long long)b.q0 * qp * 16;
     BpArgs args;
     args.vol = vol_slab;
     args.proj_bytes = proj_bytes;
@@ -322,7 +354,7 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
                  "guarded batch requires an error flag (matrix near w == 0 over the volume)");
         args.count = n;
         args.packed = static_cast<const char*>(packed) + (long long)first * proj_bytes -
-                      (long long)kMagic * 16;
+                      (long long)kMagic * 16 - band_shift;
         if (opt.mode == CBB_MODE_EXACT) {
             if (safe)
                 launch_bp_t<0, false>(args, m, nz, st);
@@ -433,6 +465,10 @@ struct Worker {
     void* d_packed_all = nullptr;
     int tail_lo = 0, tail_hi = 0;
     cudaEvent_t head_done = nullptr, tail_done = nullptr;
+    // detector rows this worker holds / packs (RowBand::full unless set_bands)
+    RowBand band;
+    size_t pk_bytes = 0;               // packed bytes per projection (band rows)
+    cudaEvent_t src_ready[2] = {};     // as root: raw slot filtered, peers may copy
 
     ~Worker() {
         if (!copy)
@@ -447,6 +483,7 @@ struct Worker {
             pool.release(device, d_packed[i]);
             cudaEventDestroy(h2d_done[i]);
             cudaEventDestroy(raw_free[i]);
+            cudaEventDestroy(src_ready[i]);
         }
         pool.release(device, d_err);
         pool.release(device, d_packed_all);
@@ -504,6 +541,7 @@ struct Pipeline {
     int slot = 0;                           // current staging / ring slot
     std::vector<double> stage_mats;         // matrices of the staged batch
     uint64_t submitted = 0;
+    uint64_t nbatch = 0;   // batches issued (root = nbatch mod workers)
     size_t raw_bytes_per_proj = 0;
     size_t packed_bytes_per_proj = 0;
     bool resident = false;         // see Worker::d_packed_all
@@ -520,12 +558,12 @@ struct Pipeline {
     void enable_resident(int count) {
         if (std::getenv("CBB_NO_RESIDENT"))
             return;
-        const size_t need = packed_bytes_per_proj * (size_t)count;
         for (auto& w : workers)
             if (w->z_end - w->z_begin < 16)
                 return;
         std::vector<void*> blocks;
         for (auto& w : workers) {
+            const size_t need = w->pk_bytes * (size_t)count;
             CK(cudaSetDevice(w->device));
             void* p = DevicePool::get().take_cached(w->device, need);
             if (!p) {
@@ -664,10 +702,13 @@ struct Pipeline {
             for (int s = 0; s < 2; ++s) {
                 CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->src_ready[s], cudaEventDisableTiming));
                 w->d_raw[s] = static_cast<float*>(
                     DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
                 w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
             }
+            w->band = RowBand::full(H);
+            w->pk_bytes = packed_bytes_per_proj;
             CK(cudaEventCreate(&w->k_beg));
             CK(cudaEventCreate(&w->k_end));
             CK(cudaEventCreate(&w->c_beg));
@@ -688,6 +729,20 @@ struct Pipeline {
             workers.push_back(std::move(w));
         }
         stage_mats.assign(12 * (size_t)opt.batch, 0.0);
+        // band copies go straight over NVLink where the devices allow it
+        for (auto& a : workers)
+            for (auto& b : workers) {
+                int can = 0;
+                if (a->device == b->device ||
+                    cudaDeviceCanAccessPeer(&can, b->device, a->device) != cudaSuccess || !can)
+                    continue;
+                CK(cudaSetDevice(b->device));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(a->device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled)
+                    cudaGetLastError();
+                else
+                    CK(e);
+            }
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             CK(cudaEventSynchronize(w->c_end));
@@ -708,34 +763,150 @@ struct Pipeline {
                              std::chrono::duration<double, std::milli>(
                                  std::chrono::steady_clock::now() - t0).count());
         }
+        // Batch k is uploaded once, by the root worker k mod G, and each
+        // other worker copies its row band from the root's raw slot (peer
+        // copy over NVLink; a plain device copy when both are one device).
+        const int G = (int)workers.size();
+        Worker& root = *workers[nbatch % G];
+        // raw[slot] of worker w may still be read by its own pack of batch
+        // k-2 and, if w was that batch's root, by the other workers' band copies
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
-            // raw[slot] may still be read by the pack of batch (k-2)
             CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
-            CK(cudaMemcpyAsync(w->d_raw[slot], src, bytes, cudaMemcpyHostToDevice, w->copy));
+            for (auto& o : workers)
+                if (o != w)
+                    CK(cudaStreamWaitEvent(w->copy, o->h2d_done[slot], 0));
+        }
+        CK(cudaSetDevice(root.device));
+        CK(cudaMemcpyAsync(root.d_raw[slot], src, bytes, cudaMemcpyHostToDevice, root.copy));
+        CK(cudaEventRecord(root.h2d_done[slot], root.copy));
+        CK(cudaStreamWaitEvent(root.compute, root.h2d_done[slot], 0));
+        start_timing(root);
+        // the root sees the whole batch: it checks the pixels its band skips
+        if (!root.band.is_full(H))
+            launch_check_finite(root.d_raw[slot], (long long)n * W * H, root.d_err, root.compute);
+        cudaEvent_t ready = root.h2d_done[slot];
+        if (opt.ramp_filter) {
+            ramp_filter_device(root.d_raw[slot], root.d_raw[slot], W, H, n, opt.filter_pixel_mm,
+                               root.compute);
+            CK(cudaEventRecord(root.src_ready[slot], root.compute));
+            ready = root.src_ready[slot];
+        }
+        for (auto& w : workers) {
+            if (w.get() == &root)
+                continue;
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamWaitEvent(w->copy, ready, 0));
+            copy_band(root, *w, slot, n);
             CK(cudaEventRecord(w->h2d_done[slot], w->copy));
             CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
-            if (!w->started) {
-                CK(cudaEventRecord(w->k_beg, w->compute));
-                w->started = true;
-            }
-            if (opt.ramp_filter)
-                ramp_filter_device(w->d_raw[slot], w->d_raw[slot], W, H, n, opt.filter_pixel_mm,
-                                   w->compute);
-            void* packed = resident ? static_cast<char*>(w->d_packed_all) +
-                                          packed_bytes_per_proj * submitted
+            start_timing(*w);
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            void* packed = resident ? static_cast<char*>(w->d_packed_all) + w->pk_bytes * submitted
                                     : w->d_packed[slot];
-            launch_pack(w->d_raw[slot], W, H, n, packed, w->compute, w->d_err);
+            if (w.get() == &root)
+                launch_pack_band(w->d_raw[slot], 0, H, (long long)W * H, W, H, n, packed, w->band,
+                                 w->compute, w->d_err);
+            else
+                launch_pack_band(w->d_raw[slot], w->band.r0, w->band.rn,
+                                 (long long)w->band.rn * W, W, H, n, packed, w->band, w->compute,
+                                 w->d_err);
             CK(cudaEventRecord(w->raw_free[slot], w->compute));
             // resident: the head, i.e. the slab minus the tail planes
             w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end, packed, W, H, n,
                                              mats, opt, w->d_err, w->compute,
-                                             resident ? w->tail_lo : 0, resident ? w->tail_hi : 0);
+                                             resident ? w->tail_lo : 0, resident ? w->tail_hi : 0,
+                                             &w->band);
         }
+        ++nbatch;
         if (resident)
             std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
         submitted += n;
         slot ^= 1;
+    }
+
+    void start_timing(Worker& w) {
+        if (!w.started) {
+            CK(cudaEventRecord(w.k_beg, w.compute));
+            w.started = true;
+        }
+    }
+
+    // Rows [band.r0, band.r0 + band.rn) of the batch's n projections, from the
+    // root's full raw slot to w's band slot (projection stride rn * W), one
+    // strided peer copy on w's copy stream.
+    void copy_band(const Worker& root, Worker& w, int s, int n) {
+        const RowBand& b = w.band;
+        if (b.rn <= 0)
+            return;
+        cudaMemcpy3DPeerParms p = {};
+        const size_t row_bytes = (size_t)b.rn * W * sizeof(float);
+        p.srcPtr = make_cudaPitchedPtr(root.d_raw[s] + (size_t)b.r0 * W, raw_bytes_per_proj,
+                                       row_bytes, n);
+        p.srcDevice = root.device;
+        p.dstPtr = make_cudaPitchedPtr(w.d_raw[s], row_bytes, row_bytes, n);
+        p.dstDevice = w.device;
+        p.extent = make_cudaExtent(row_bytes, n, 1);
+        CK(cudaMemcpy3DPeerAsync(&p, w.copy));
+    }
+
+    // The detector rows worker w's voxels can touch over the whole stack: the
+    // slab box's 8 corners projected (w > 0 over the box makes v/w extremal
+    // at corners), 2 cells of margin, and the rows -2 / H the clamped
+    // gathers fall back to when the footprint leaves the detector. The kernel
+    // computes padding voxels at real ones, so nothing outside is read.
+    RowBand band_for(const Worker& w, const double* mats, int count) const {
+        const RowBand full = RowBand::full(H);
+        if (std::getenv("CBB_NO_BANDS"))
+            return full;
+        const int L = g.edge_voxels;
+        const double xs[2] = {g.origin_mm, g.origin_mm + (L - 1) * g.voxel_mm};
+        const double zs[2] = {g.origin_mm + w.z_begin * g.voxel_mm,
+                              g.origin_mm + (w.z_end - 1) * g.voxel_mm};
+        double lo = 1e300, hi = -1e300;
+        for (int p = 0; p < count; ++p) {
+            const double* a = mats + 12 * (size_t)p;
+            for (int c = 0; c < 8; ++c) {
+                const double x = xs[c & 1], y = xs[(c >> 1) & 1], z = zs[c >> 2];
+                const double v = a[1] * x + a[4] * y + a[7] * z + a[10];
+                const double ww = a[2] * x + a[5] * y + a[8] * z + a[11];
+                if (!(ww > 0.0))
+                    return full;
+                lo = std::min(lo, v / ww);
+                hi = std::max(hi, v / ww);
+            }
+        }
+        if (!(lo > -1e7 && hi < 1e7))
+            return full;
+        const long long fl = (long long)std::floor(lo), fh = (long long)std::floor(hi);
+        auto clampll = [](long long v, long long a, long long b) {
+            return std::min(std::max(v, a), b);
+        };
+        const long long c0 = std::min(std::max(fl - 2, (long long)-kPad), clampll(fl - 2, -2, H));
+        const long long c1 =
+            std::max(std::min(fh + 2, (long long)H + kPad - 1), clampll(fh + 2, -2, H));
+        RowBand b;
+        b.q0 = (int)(c0 + kPad);
+        b.qn = (int)(c1 - c0 + 1);
+        b.r0 = (int)std::max(0LL, c0);
+        b.rn = (int)std::max(0LL, std::min<long long>(H, c1 + 2) - b.r0);
+        if (b.qn >= full.qn)
+            return full;
+        return b;
+    }
+
+    // Sets every worker's row band for a stack whose matrices are all known.
+    void set_bands(const double* mats, int count) {
+        for (auto& w : workers) {
+            w->band = band_for(*w, mats, count);
+            w->pk_bytes = (size_t)quad_pitch_cells(W) * w->band.qn * 16;
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: device %d slab [%d, %d) rows [%d, %d) cells %d of %d\n",
+                             w->device, w->z_begin, w->z_end, w->band.r0,
+                             w->band.r0 + w->band.rn, w->band.qn, quad_rows(H));
+        }
     }
 
     // Host-side proof that every batch of the tail pass runs unguarded (no
@@ -800,6 +971,7 @@ struct Pipeline {
     void submit_stack(const float* imgs, const double* mats, int count) {
         if (submitted == 0) {
             const auto t0 = std::chrono::steady_clock::now();
+            set_bands(mats, count);
             enable_resident(count);
             if (std::getenv("CBB_TRACE"))
                 std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
@@ -957,7 +1129,7 @@ struct Pipeline {
                 w->guarded += launch_backproject(
                     w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
                     w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
-                    w->compute);
+                    w->compute, 0, 0, &w->band);
                 continue;
             }
             // head out now; the tail copied out as soon as it is computed (no
@@ -968,7 +1140,7 @@ struct Pipeline {
             CK(cudaEventRecord(w->head_done, w->copy));
             launch_backproject(w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo,
                                w->tail_hi, w->d_packed_all, W, H, resident_count,
-                               all_mats.data(), opt, w->d_err, w->compute);
+                               all_mats.data(), opt, w->d_err, w->compute, 0, 0, &w->band);
             CK(cudaEventRecord(w->tail_done, w->compute));
             CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
             d2h(*w, w->tail_lo, w->tail_hi);
