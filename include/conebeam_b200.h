@@ -185,6 +185,49 @@ cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* ge
                                   const double* mats, const cbb_options* options,
                                   int32_t* err_flag, void* stream);
 
+/* Row bands (multi-GPU z-slabs): the detector rows a slab's voxels can touch
+ * over a set of projections. A worker then holds only those raw rows and
+ * packs only the matching cell rows (cell row = detector row + pad, see
+ * cbb_packed_layout); at 8 slabs of a 512^3 volume each needs about a third of
+ * the detector. Full detector (raw 0..H, cells 0..quad_rows) when w <= 0
+ * somewhere on the slab or the rows are unbounded. */
+typedef struct cbb_row_band {
+    int32_t raw_row0;  /* detector rows held: [raw_row0, raw_row0 + raw_rows) */
+    int32_t raw_rows;
+    int32_t cell_row0; /* packed cell rows: [cell_row0, cell_row0 + cell_rows) */
+    int32_t cell_rows;
+} cbb_row_band;
+
+cbb_status cbb_row_band_for_slab(const cbb_volume_geometry* geometry, int32_t width,
+                                 int32_t height, int32_t z_begin, int32_t z_end,
+                                 const double* mats, int32_t count, cbb_row_band* band);
+
+/* Packs count projections, band cell rows only (band->cell_rows * quad_pitch
+ * float4 cells each). raw points at detector row band->raw_row0 of projection
+ * 0; consecutive projections are raw_stride floats apart (width*height for a
+ * full raw buffer offset by raw_row0*width, raw_rows*width for a band
+ * buffer). Pixels outside the held rows read as 0. err_flag (device int,
+ * nullable): bit 2 set on a non-finite pixel among the packed ones. */
+cbb_status cbb_pack_device_band(const float* raw, int64_t raw_stride, int32_t width,
+                                int32_t height, int32_t count, const cbb_row_band* band,
+                                void* packed, int32_t* err_flag, void* stream);
+
+/* cbb_backproject_device on band-packed projections. band must cover the
+ * footprint of [z_begin, z_end) for these matrices (checked on the host:
+ * CBB_ERR_INVALID otherwise); NULL = full detector. */
+cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometry* geometry,
+                                       int32_t z_begin, int32_t z_end, const void* packed,
+                                       int32_t width, int32_t height, int32_t count,
+                                       const double* mats, const cbb_row_band* band,
+                                       const cbb_options* options, int32_t* err_flag,
+                                       void* stream);
+
+/* ProjectionImage::validate on the device (proj/src/dataset.cpp:123-129):
+ * sets bit 2 of *err_flag if any of the n floats is not finite. For the
+ * uploading rank of a row-band pipeline, whose own band skips rows. */
+cbb_status cbb_check_finite_device(const float* values, int64_t n, int32_t* err_flag,
+                                   void* stream);
+
 /* FDK filtering step (upstream of the back-projection; the reference consumes
  * pre-filtered data): row-wise Shepp-Logan ramp filter
  * h[n] = -2/(pi^2 tau (4n^2-1)) as a linear convolution (zero-padded float64

@@ -22,8 +22,14 @@ EXPORTS = (
     "cbb_session_free", "cbb_packed_layout", "cbb_pack_device",
     "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
     "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
-    "cbb_backproject_texture_device",
+    "cbb_backproject_texture_device", "cbb_row_band_for_slab", "cbb_pack_device_band",
+    "cbb_backproject_device_band", "cbb_check_finite_device",
 )
+
+
+class RowBandC(C.Structure):
+    _fields_ = [("raw_row0", C.c_int32), ("raw_rows", C.c_int32),
+                ("cell_row0", C.c_int32), ("cell_rows", C.c_int32)]
 
 
 class StackFileInfoC(C.Structure):
@@ -126,6 +132,20 @@ def _declare(L) -> None:
     L.cbb_compare_volumes_device.restype = C.c_int
     L.cbb_compare_volumes_device.argtypes = [_VP, _VP, C.c_int64, C.c_double,
                                              C.POINTER(VolumeDiffC), _VP]
+    L.cbb_row_band_for_slab.restype = C.c_int
+    L.cbb_row_band_for_slab.argtypes = [C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_int32, _VP, C.c_int32,
+                                        C.POINTER(RowBandC)]
+    L.cbb_pack_device_band.restype = C.c_int
+    L.cbb_pack_device_band.argtypes = [_VP, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(RowBandC), _VP, _VP, _VP]
+    L.cbb_backproject_device_band.restype = C.c_int
+    L.cbb_backproject_device_band.argtypes = [_VP, C.POINTER(VolumeGeometryC), C.c_int32,
+                                              C.c_int32, _VP, C.c_int32, C.c_int32, C.c_int32,
+                                              _VP, C.POINTER(RowBandC), C.POINTER(OptionsC),
+                                              _VP, _VP]
+    L.cbb_check_finite_device.restype = C.c_int
+    L.cbb_check_finite_device.argtypes = [_VP, C.c_int64, _VP, _VP]
     L.cbb_launch_count.restype = C.c_uint64
     L.cbb_launch_count.argtypes = []
 

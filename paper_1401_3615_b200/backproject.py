@@ -258,12 +258,76 @@ def pack_device(raw, packed, stream=None) -> None:
                                           C.c_void_p(s.cuda_stream)))
 
 
+@dataclass(frozen=True)
+class RowBand:
+    """Detector rows [raw_row0, raw_row0 + raw_rows) a z-slab's voxels can
+    touch, and the packed cell rows [cell_row0, cell_row0 + cell_rows) holding
+    them (cbb_row_band_for_slab)."""
+    raw_row0: int
+    raw_rows: int
+    cell_row0: int
+    cell_rows: int
+
+    def c(self):
+        return _lib.RowBandC(self.raw_row0, self.raw_rows, self.cell_row0, self.cell_rows)
+
+    def packed_bytes(self, width: int, height: int) -> int:
+        qp, _, _ = packed_layout(width, height)
+        return qp * self.cell_rows * 16
+
+
+def row_band_for_slab(geometry: VolumeGeometry, width: int, height: int, z_begin: int,
+                      z_end: int, matrices: np.ndarray) -> RowBand:
+    """Row band of slab [z_begin, z_end) over these projections."""
+    m = validate_matrices(matrices)
+    b = _lib.RowBandC()
+    _lib.check(_lib.lib().cbb_row_band_for_slab(C.byref(geometry_c(geometry)), int(width),
+                                                int(height), int(z_begin), int(z_end), _ptr(m),
+                                                m.shape[0], C.byref(b)))
+    return RowBand(b.raw_row0, b.raw_rows, b.cell_row0, b.cell_rows)
+
+
+def pack_device_band(raw, band: RowBand, packed, err_flag=None, stream=None,
+                     height: Optional[int] = None) -> None:
+    """Packs the band's cell rows of raw projections (cbb_pack_device_band).
+    raw: CUDA float32 (N, rows, W) holding detector rows from band.raw_row0 on
+    -- either the full detector (rows == height; pass height=None) or just the
+    band (rows == band.raw_rows; pass the detector height)."""
+    import torch
+
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
+        raise ValidationError("pack_device_band: raw must be a contiguous CUDA float32 (N, R, W) tensor")
+    n, rows, w = raw.shape
+    h = rows if height is None else int(height)
+    ptr = raw.data_ptr()
+    if height is None:  # full buffer: start at the band's first row
+        ptr += band.raw_row0 * w * 4
+    if packed.numel() * packed.element_size() < n * band.packed_bytes(w, h):
+        raise ValidationError("pack_device_band: packed buffer too small")
+    s = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    _lib.check(_lib.lib().cbb_pack_device_band(
+        ptr, rows * w, w, h, n, C.byref(band.c()), packed.data_ptr(),
+        None if err_flag is None else err_flag.data_ptr(), C.c_void_p(s.cuda_stream)))
+
+
+def check_finite_device(values, err_flag, stream=None) -> None:
+    """Sets bit 2 of err_flag (device int32) if a value is not finite."""
+    import torch
+
+    if not (values.is_cuda and values.dtype == torch.float32 and values.is_contiguous()):
+        raise ValidationError("check_finite_device: contiguous CUDA float32 tensor")
+    s = stream if stream is not None else torch.cuda.current_stream(values.device)
+    _lib.check(_lib.lib().cbb_check_finite_device(values.data_ptr(), values.numel(),
+                                                  err_flag.data_ptr(), C.c_void_p(s.cuda_stream)))
+
+
 def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: int, packed,
                        width: int, height: int, count: int, matrices: np.ndarray,
                        options: Optional[Options] = None, err_flag=None, stream=None,
-                       first: int = 0) -> None:
+                       first: int = 0, band: Optional[RowBand] = None) -> None:
     """Enqueues the back-projection of `count` packed projections (starting at
-    packed projection `first`) into a device z-slab [z_begin, z_end)."""
+    packed projection `first`) into a device z-slab [z_begin, z_end); with
+    `band`, the projections were packed by pack_device_band with that band."""
     import torch
 
     if not (vol_slab.is_cuda and vol_slab.dtype == torch.float32 and vol_slab.is_contiguous()):
@@ -278,11 +342,18 @@ def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: 
     oc, _keep = (options or Options()).to_c()
     g = geometry_c(geometry)
     s = stream if stream is not None else torch.cuda.current_stream(vol_slab.device)
-    _lib.check(_lib.lib().cbb_backproject_device(
+    err = None if err_flag is None else err_flag.data_ptr()
+    if band is None:
+        _lib.check(_lib.lib().cbb_backproject_device(
+            vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end),
+            packed.data_ptr() + int(first) * nb, int(width), int(height), int(count), _ptr(m),
+            C.byref(oc), err, C.c_void_p(s.cuda_stream)))
+        return
+    nbb = band.packed_bytes(width, height)
+    _lib.check(_lib.lib().cbb_backproject_device_band(
         vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end),
-        packed.data_ptr() + int(first) * nb, int(width), int(height), int(count), _ptr(m),
-        C.byref(oc), None if err_flag is None else err_flag.data_ptr(),
-        C.c_void_p(s.cuda_stream)))
+        packed.data_ptr() + int(first) * nbb, int(width), int(height), int(count), _ptr(m),
+        C.byref(band.c()), C.byref(oc), err, C.c_void_p(s.cuda_stream)))
 
 
 def ramp_filter_device(raw, out, pixel_mm: float, stream=None) -> None:

@@ -234,6 +234,52 @@ struct RowBand {
     bool is_full(int H) const { return r0 == 0 && rn == H && q0 == 0 && qn == quad_rows(H); }
 };
 
+// The detector rows the voxels of slab [z_begin, z_end) can touch for the
+// given projections: the slab box's 8 corners projected (w > 0 over the box
+// makes v/w extremal at corners), 2 cells of margin, and the rows -2 / H the
+// clamped gathers fall back to when a footprint leaves the detector. The
+// kernel computes padding voxels at real ones, so nothing outside is read.
+// Full band when w <= 0 somewhere on the box or the rows are unbounded.
+RowBand row_band_for(const cbb_volume_geometry& g, int W, int H, int z_begin, int z_end,
+                     const double* mats, int count) {
+    (void)W;
+    const RowBand full = RowBand::full(H);
+    const int L = g.edge_voxels;
+    const double xs[2] = {g.origin_mm, g.origin_mm + (L - 1) * g.voxel_mm};
+    const double zs[2] = {g.origin_mm + z_begin * g.voxel_mm,
+                          g.origin_mm + (z_end - 1) * g.voxel_mm};
+    double lo = 1e300, hi = -1e300;
+    for (int p = 0; p < count; ++p) {
+        const double* a = mats + 12 * (size_t)p;
+        for (int c = 0; c < 8; ++c) {
+            const double x = xs[c & 1], y = xs[(c >> 1) & 1], z = zs[c >> 2];
+            const double v = a[1] * x + a[4] * y + a[7] * z + a[10];
+            const double ww = a[2] * x + a[5] * y + a[8] * z + a[11];
+            if (!(ww > 0.0))
+                return full;
+            lo = std::min(lo, v / ww);
+            hi = std::max(hi, v / ww);
+        }
+    }
+    if (!(lo > -1e7 && hi < 1e7))
+        return full;
+    const long long fl = (long long)std::floor(lo), fh = (long long)std::floor(hi);
+    auto clampll = [](long long v, long long a, long long b) {
+        return std::min(std::max(v, a), b);
+    };
+    const long long c0 = std::min(std::max(fl - 2, (long long)-kPad), clampll(fl - 2, -2, H));
+    const long long c1 =
+        std::max(std::min(fh + 2, (long long)H + kPad - 1), clampll(fh + 2, -2, H));
+    RowBand b;
+    b.q0 = (int)(c0 + kPad);
+    b.qn = (int)(c1 - c0 + 1);
+    b.r0 = (int)std::max(0LL, c0);
+    b.rn = (int)std::max(0LL, std::min<long long>(H, c1 + 2) - b.r0);
+    if (b.qn >= full.qn)
+        return full;
+    return b;
+}
+
 // Packs `count` projections whose raw rows [band.r0, band.r0 + band.rn) lie
 // raw_stride floats apart (band.rn * W for a band buffer, W * H for a full one
 // with raw pointing at row 0 -- then pass raw_row0 = 0, raw_rows = H).
@@ -852,49 +898,10 @@ struct Pipeline {
         CK(cudaMemcpy3DPeerAsync(&p, w.copy));
     }
 
-    // The detector rows worker w's voxels can touch over the whole stack: the
-    // slab box's 8 corners projected (w > 0 over the box makes v/w extremal
-    // at corners), 2 cells of margin, and the rows -2 / H the clamped
-    // gathers fall back to when the footprint leaves the detector. The kernel
-    // computes padding voxels at real ones, so nothing outside is read.
     RowBand band_for(const Worker& w, const double* mats, int count) const {
-        const RowBand full = RowBand::full(H);
         if (std::getenv("CBB_NO_BANDS"))
-            return full;
-        const int L = g.edge_voxels;
-        const double xs[2] = {g.origin_mm, g.origin_mm + (L - 1) * g.voxel_mm};
-        const double zs[2] = {g.origin_mm + w.z_begin * g.voxel_mm,
-                              g.origin_mm + (w.z_end - 1) * g.voxel_mm};
-        double lo = 1e300, hi = -1e300;
-        for (int p = 0; p < count; ++p) {
-            const double* a = mats + 12 * (size_t)p;
-            for (int c = 0; c < 8; ++c) {
-                const double x = xs[c & 1], y = xs[(c >> 1) & 1], z = zs[c >> 2];
-                const double v = a[1] * x + a[4] * y + a[7] * z + a[10];
-                const double ww = a[2] * x + a[5] * y + a[8] * z + a[11];
-                if (!(ww > 0.0))
-                    return full;
-                lo = std::min(lo, v / ww);
-                hi = std::max(hi, v / ww);
-            }
-        }
-        if (!(lo > -1e7 && hi < 1e7))
-            return full;
-        const long long fl = (long long)std::floor(lo), fh = (long long)std::floor(hi);
-        auto clampll = [](long long v, long long a, long long b) {
-            return std::min(std::max(v, a), b);
-        };
-        const long long c0 = std::min(std::max(fl - 2, (long long)-kPad), clampll(fl - 2, -2, H));
-        const long long c1 =
-            std::max(std::min(fh + 2, (long long)H + kPad - 1), clampll(fh + 2, -2, H));
-        RowBand b;
-        b.q0 = (int)(c0 + kPad);
-        b.qn = (int)(c1 - c0 + 1);
-        b.r0 = (int)std::max(0LL, c0);
-        b.rn = (int)std::max(0LL, std::min<long long>(H, c1 + 2) - b.r0);
-        if (b.qn >= full.qn)
-            return full;
-        return b;
+            return RowBand::full(H);
+        return row_band_for(g, W, H, w.z_begin, w.z_end, mats, count);
     }
 
     // Sets every worker's row band for a stack whose matrices are all known.
@@ -1419,6 +1426,102 @@ cbb_status cbb_backproject_device(float* vol_slab, const cbb_volume_geometry* ge
         const cbb_options opt = resolve_options(options);
         launch_backproject(vol_slab, *geometry, z_begin, z_end, packed, width, height, count,
                            mats, opt, err_flag, static_cast<cudaStream_t>(stream));
+    });
+}
+
+namespace {
+RowBand band_from_c(const cbb_row_band* b, int H) {
+    if (!b)
+        return RowBand::full(H);
+    RowBand r;
+    r.r0 = b->raw_row0;
+    r.rn = b->raw_rows;
+    r.q0 = b->cell_row0;
+    r.qn = b->cell_rows;
+    if (r.r0 < 0 || r.rn < 0 || r.r0 + r.rn > H || r.q0 < 0 || r.qn < 1 ||
+        r.q0 + r.qn > quad_rows(H))
+        fail(CBB_ERR_INVALID, "row band [%d, +%d) rows / [%d, +%d) cells outside the detector",
+             r.r0, r.rn, r.q0, r.qn);
+    return r;
+}
+} // namespace
+
+cbb_status cbb_row_band_for_slab(const cbb_volume_geometry* geometry, int32_t width,
+                                 int32_t height, int32_t z_begin, int32_t z_end,
+                                 const double* mats, int32_t count, cbb_row_band* band) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (!mats || !band || count < 1)
+            fail(CBB_ERR_INVALID, "cbb_row_band_for_slab: null argument or count < 1");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin >= z_end)
+            fail(CBB_ERR_INVALID, "cbb_row_band_for_slab: bad slab [%d, %d)", z_begin, z_end);
+        validate_matrices(mats, count);
+        const RowBand b = row_band_for(*geometry, width, height, z_begin, z_end, mats, count);
+        band->raw_row0 = b.r0;
+        band->raw_rows = b.rn;
+        band->cell_row0 = b.q0;
+        band->cell_rows = b.qn;
+    });
+}
+
+cbb_status cbb_pack_device_band(const float* raw, int64_t raw_stride, int32_t width,
+                                int32_t height, int32_t count, const cbb_row_band* band,
+                                void* packed, int32_t* err_flag, void* stream) {
+    return guarded([&] {
+        validate_detector(width, height);
+        if (!raw || !packed || !band || count < 0)
+            fail(CBB_ERR_INVALID, "cbb_pack_device_band: null argument");
+        if (count > 65535)
+            fail(CBB_ERR_INVALID, "cbb_pack_device_band: count > 65535 per call");
+        const RowBand b = band_from_c(band, height);
+        if (raw_stride < (int64_t)b.rn * width)
+            fail(CBB_ERR_INVALID, "cbb_pack_device_band: raw_stride below the band size");
+        if (count == 0)
+            return;
+        launch_pack_band(raw, b.r0, b.rn, raw_stride, width, height, count, packed, b,
+                         static_cast<cudaStream_t>(stream), err_flag);
+    });
+}
+
+cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometry* geometry,
+                                       int32_t z_begin, int32_t z_end, const void* packed,
+                                       int32_t width, int32_t height, int32_t count,
+                                       const double* mats, const cbb_row_band* band,
+                                       const cbb_options* options, int32_t* err_flag,
+                                       void* stream) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (!vol_slab || !packed || !mats)
+            fail(CBB_ERR_INVALID, "cbb_backproject_device_band: null argument");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin > z_end)
+            fail(CBB_ERR_INVALID, "cbb_backproject_device_band: bad slab [%d, %d)", z_begin,
+                 z_end);
+        validate_matrices(mats, count);
+        const RowBand b = band_from_c(band, height);
+        if (band && z_end > z_begin && count > 0) {
+            const RowBand need =
+                row_band_for(*geometry, width, height, z_begin, z_end, mats, count);
+            if (need.q0 < b.q0 || need.q0 + need.qn > b.q0 + b.qn ||
+                (need.rn > 0 && (need.r0 < b.r0 || need.r0 + need.rn > b.r0 + b.rn)))
+                fail(CBB_ERR_INVALID,
+                     "cbb_backproject_device_band: band cells [%d, %d) do not cover the "
+                     "slab's footprint [%d, %d)",
+                     b.q0, b.q0 + b.qn, need.q0, need.q0 + need.qn);
+        }
+        const cbb_options opt = resolve_options(options);
+        launch_backproject(vol_slab, *geometry, z_begin, z_end, packed, width, height, count,
+                           mats, opt, err_flag, static_cast<cudaStream_t>(stream), 0, 0, &b);
+    });
+}
+
+cbb_status cbb_check_finite_device(const float* values, int64_t n, int32_t* err_flag,
+                                   void* stream) {
+    return guarded([&] {
+        if (!values || !err_flag || n < 0)
+            fail(CBB_ERR_INVALID, "cbb_check_finite_device: null argument");
+        launch_check_finite(values, n, err_flag, static_cast<cudaStream_t>(stream));
     });
 }
 

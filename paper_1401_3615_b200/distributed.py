@@ -79,26 +79,55 @@ def batch_roots(count: int, batch: int, world: int) -> List[tuple]:
 
 @dataclass
 class Hooks:
-    """Compute hooks: pack(raw (n,H,W), packed) and
-    backproject(vol_slab, z0, z1, packed, n, mats)."""
+    """Compute hooks: pack(raw (n,H,W) full detector, packed, err),
+    backproject(vol_slab, z0, z1, packed, n, mats, err), packed bytes per
+    projection; check(raw, err) scans a whole uploaded batch (the uploading
+    rank runs it when its own pack skips rows); for_stack(z0, z1, mats)
+    returns hooks specialised to one stack (the slab's row band)."""
     pack: Callable
     backproject: Callable
     packed_bytes: int
+    check: Optional[Callable] = None
+    for_stack: Optional[Callable] = None
 
 
-def cuda_hooks(geometry: VolumeGeometry, width: int, height: int, options=None) -> Hooks:
-    from .backproject import backproject_device, pack_device, packed_layout
+def cuda_hooks(geometry: VolumeGeometry, width: int, height: int, options=None,
+               band=None) -> Hooks:
+    """CUDA hooks over the C ABI. With band (RowBand), each rank packs only
+    the detector rows its slab projects onto (cbb_pack_device_band) and the
+    kernel reads that band; for_stack picks the band for a stack."""
+    from .backproject import (backproject_device, check_finite_device, pack_device,
+                              pack_device_band, packed_layout, row_band_for_slab)
 
     _, _, nb = packed_layout(width, height)
 
-    def pack(raw, packed):
-        pack_device(raw, packed)
+    def for_stack(z0, z1, mats):
+        b = row_band_for_slab(geometry, width, height, z0, z1, mats)
+        return cuda_hooks(geometry, width, height, options, band=b)
 
-    def back(vol_slab, z0, z1, packed, n, mats, err):
+    if band is None:
+        def pack(raw, packed, err):
+            pack_device(raw, packed)
+
+        def back(vol_slab, z0, z1, packed, n, mats, err):
+            backproject_device(vol_slab, geometry, z0, z1, packed, width, height, n, mats,
+                               options, err_flag=err)
+
+        return Hooks(pack, back, nb, None, for_stack)
+
+    def pack_b(raw, packed, err):
+        pack_device_band(raw, band, packed, err_flag=err)
+
+    def back_b(vol_slab, z0, z1, packed, n, mats, err):
         backproject_device(vol_slab, geometry, z0, z1, packed, width, height, n, mats,
-                           options, err_flag=err)
+                           options, err_flag=err, band=band)
 
-    return Hooks(pack, back, nb)
+    def check(raw, err):
+        check_finite_device(raw, err)
+
+    full = band.cell_row0 == 0 and band.cell_rows == packed_layout(width, height)[1]
+    return Hooks(pack_b, back_b, band.packed_bytes(width, height), None if full else check,
+                 for_stack)
 
 
 class DistributedReconstructor:
@@ -171,6 +200,11 @@ class DistributedReconstructor:
 
         m = validate_matrices(mats)
         count = m.shape[0]
+        hooks = self.hooks
+        if hooks.for_stack is not None:
+            hooks = hooks.for_stack(self.z0, self.z1, m)
+            if hooks.packed_bytes > self.hooks.packed_bytes:
+                raise ValueError("stack hooks need larger packed buffers")
         if initial_slab is not None:
             self.vol.copy_(torch.as_tensor(np.ascontiguousarray(initial_slab)))
         else:
@@ -188,11 +222,22 @@ class DistributedReconstructor:
                     torch.cuda.current_stream(self.device).wait_event(pending)
                 else:
                     pending.wait()
-            self.hooks.pack(self.raw[slot][:n], self.packed[slot])
-            self.hooks.backproject(self.vol, self.z0, self.z1, self.packed[slot], n,
-                                   m[first:first + n], self.err)
+            if root == self.rank and hooks.check is not None:
+                hooks.check(self.raw[slot][:n], self.err)
+            hooks.pack(self.raw[slot][:n], self.packed[slot], self.err)
+            hooks.backproject(self.vol, self.z0, self.z1, self.packed[slot], n,
+                              m[first:first + n], self.err)
             pending = nxt
-        if int(self.err.item()) != 0:
+        # every rank raises the same error: OR of the flags (bit 1: w == 0,
+        # bit 2: non-finite pixel) over the group
+        flags = torch.stack([(self.err & 1) != 0, (self.err & 2) != 0]).to(torch.int32)
+        if self.world > 1:
+            self.dist.all_reduce(flags, op=self.dist.ReduceOp.MAX, group=self.group)
+        flags = flags.cpu().reshape(-1).tolist()
+        if flags[1]:
+            from .errors import ValidationError
+            raise ValidationError("ProjectionImage contains non-finite values")
+        if flags[0]:
             from .errors import GeometryError
             raise GeometryError("backprojection hit a voxel with w == 0")
         out = torch.empty(self.vol.shape, dtype=torch.float32,

@@ -21,7 +21,7 @@ L, W, H, N, BATCH = 12, 7, 5, 11, 3
 def stub_hooks():
     nb = W * H * 4
 
-    def pack(raw, packed):
+    def pack(raw, packed, err):
         n = raw.shape[0]
         packed[: n * nb].copy_(raw.reshape(-1).view(torch.uint8))
 
@@ -116,3 +116,50 @@ def test_slab_plans():
         assert max(per) / (sum(per) / world) < 1.05
         eq = [work[a:b].sum() for a, b in D.equal_slabs(512, world)]
         assert max(per) <= max(eq)
+
+
+def error_worker(rank, world, port, q):
+    """Rank 1's slab flags w == 0 in one batch; rank 0 flags nothing. Both
+    ranks must raise the same error (flags are OR-reduced over the group), and
+    the uploading rank alone scans each batch (Hooks.check)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        imgs, mats = data()
+        base = stub_hooks()
+        checked = []
+
+        def back(vol, z0, z1, packed, n, m, err):
+            base.backproject(vol, z0, z1, packed, n, m, err)
+            if z0 > 0 and np.any(np.asarray(m)[:, 0] == mats[4][0]):
+                err |= 1
+
+        def check(raw, err):
+            checked.append(int(raw.shape[0]))
+
+        hooks = D.Hooks(base.pack, back, base.packed_bytes, check)
+        rec = D.DistributedReconstructor(VolumeGeometry.centered(L, 1.0), W, H, batch=BATCH,
+                                         device="cpu", hooks=hooks)
+        try:
+            rec.reconstruct(torch.from_numpy(imgs), mats)
+            q.put((rank, "no error", checked))
+        except Exception as e:  # noqa: BLE001
+            q.put((rank, type(e).__name__, checked))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_errors_reach_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=error_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [o[1] for o in out] == ["GeometryError", "GeometryError"]
+    # batches of 3 over 11 projections: roots 0, 1, 0, 1 -> sizes (3, 3) / (3, 2)
+    assert out[0][2] == [3, 3] and out[1][2] == [3, 2]

@@ -155,6 +155,33 @@ def test_distributed_driver_single_rank(cuda):
     assert bits_equal(rec.gather(slab), expected)
 
 
+@pytest.mark.parametrize("z0,z1", [(0, 9), (24, 40), (56, 64)])
+def test_distributed_driver_row_band_slab(cuda, oracle, z0, z1):
+    """The torch.distributed driver owning one narrow slab packs only its row
+    band (cbb_row_band_for_slab -> cbb_pack_device_band ->
+    cbb_backproject_device_band): bitwise the oracle's planes; a NaN in a row
+    outside the band is still caught by the uploading rank's full scan."""
+    import torch
+
+    from paper_1401_3615_b200.distributed import DistributedReconstructor
+
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=30)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=15)
+    imgs = imgs_t.numpy()
+    ref = np.zeros((64,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    band = pkg.row_band_for_slab(g, cfg.width, cfg.height, z0, z1, mats)
+    assert band.raw_rows < cfg.height
+    rec = DistributedReconstructor(g, cfg.width, cfg.height, batch=8, slabs=[(z0, z1)])
+    slab = rec.reconstruct(torch.from_numpy(imgs).pin_memory(), mats)
+    assert bits_equal(slab, ref[z0:z1])
+    bad = imgs.copy()
+    row = 0 if band.raw_row0 > 0 else cfg.height - 1
+    bad[9, row, 3] = np.inf
+    with pytest.raises(pkg.ValidationError):
+        rec.reconstruct(torch.from_numpy(bad).pin_memory(), mats)
+
+
 def test_single_process_multi_worker_slabs(cuda):
     """cbb_reconstruct with several workers (one z-slab each): device_ids
     [0, 0, 0] runs three independent slab pipelines on one GPU (no kernel

@@ -219,3 +219,49 @@ def test_stack_file_query_error_mapping(tmp_path):
             pkg.stack_file_info(p)
     with pytest.raises(pkg.IOError_):
         pkg.stack_file_info(str(tmp_path / "missing.cbps"))
+
+
+def test_row_bands_cover_every_tap():
+    """cbb_row_band_for_slab (host-side, no GPU): for 8 z-slabs of a scan, the
+    band's cell rows contain the cell of every voxel x projection tap the
+    kernel can read (trunc(iy), clamped to [-2, H] off the margin), its raw
+    rows every detector row those cells hold, and it is narrower than the
+    detector; a projection with w <= 0 on the slab gives the full detector."""
+    import paper_1401_3615_b200 as pkg
+    from paper_1401_3615_b200 import synth
+
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=62)
+    g = cfg.geometry
+    mats = synth.perturbed_matrices(cfg)
+    W, H = cfg.width, cfg.height
+    qp, qr, _ = pkg.packed_layout(W, H)
+    pad = (qr - H) // 2
+    L = g.edge_voxels
+    rng = np.random.default_rng(3)
+    for z0 in range(0, L, 8):
+        z1 = z0 + 8
+        b = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
+        assert b.cell_rows < qr
+        idx = rng.integers(0, L, size=(3000, 2))
+        zi = rng.integers(z0, z1, size=3000)
+        corners = np.array([[x, y, z] for x in (0, L - 1) for y in (0, L - 1) for z in (z0, z1 - 1)])
+        pts = np.concatenate([np.stack([idx[:, 0], idx[:, 1], zi], 1), corners])
+        wpt = g.origin_mm + pts * g.voxel_mm
+        hom = np.concatenate([wpt, np.ones((len(pts), 1))], 1)
+        for a in mats:
+            A = a.reshape(4, 3).T  # column-major 3x4
+            u, v, w = A @ hom.T
+            assert np.all(w > 0)
+            iy = np.trunc(v / w)
+            inside = (iy >= -pad) & (iy <= H + pad - 2)
+            cell = np.where(inside, iy, np.clip(iy, -2, H)) + pad
+            assert cell.min() >= b.cell_row0 and cell.max() < b.cell_row0 + b.cell_rows
+        rows_needed = [r for c in range(b.cell_row0 - pad, b.cell_row0 + b.cell_rows - pad)
+                       for r in (c, c + 1) if 0 <= r < H]
+        if rows_needed:
+            assert min(rows_needed) >= b.raw_row0
+            assert max(rows_needed) < b.raw_row0 + b.raw_rows
+    bad = mats.copy()
+    bad[5, 11] = -5.0  # w(0) < 0 for projection 5
+    full = pkg.row_band_for_slab(g, W, H, 0, 8, bad)
+    assert (full.raw_row0, full.raw_rows, full.cell_row0, full.cell_rows) == (0, H, 0, qr)
