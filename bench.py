@@ -261,8 +261,11 @@ def run_ours(args):
     else:
         slabs = [(0, L)]
     z0, z1 = slabs[rank]
-    _, _, nb = pkg.packed_layout(W, H)
-    packed = torch.empty(n * nb, dtype=torch.uint8, device=dev)
+    # this rank packs only the detector rows its slab projects onto (the
+    # whole detector for a single 512^3 slab)
+    band = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
+    nb = band.packed_bytes(W, H)
+    packed = torch.empty(n * pkg.packed_layout(W, H)[2], dtype=torch.uint8, device=dev)
     vol = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -275,10 +278,11 @@ def run_ours(args):
         vol.zero_()
         if i is not None:
             ev[i][0].record(stream)
-        pkg.pack_device(imgs, packed, stream)
+        pkg.pack_device_band(imgs, band, packed, err, stream)
         if i is not None:
             ev[i][1].record(stream)
-        pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream)
+        pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream,
+                               band=band)
         if i is not None:
             ev[i][2].record(stream)
 
@@ -361,6 +365,8 @@ def run_ours(args):
                    "projections": n, "detector": [W, H], "mode": args.mode,
                    "batch": args.batch, "parallelism": f"z-slab x{world}",
                    "slabs": [list(s) for s in slabs],
+                   "row_band": {"rows": [band.raw_row0, band.raw_row0 + band.raw_rows],
+                                "cell_rows": band.cell_rows},
                    "l2": (f"inputs larger than L2 ({imgs.numel() * 4 / 1e9:.1f} GB raw + "
                           f"{n * nb / 1e9:.1f} GB packed vs 0.126 GB L2), no flush")},
         "pack_ms_per_step": round(statistics.mean(pack_ms), 4),
@@ -380,10 +386,13 @@ def run_ours(args):
             v2 = torch.empty(((zz1 - zz0), LL, LL), dtype=torch.float32, device=dev)
             o2 = pkg.Options(batch=args.batch, mode=mode_id)
 
+            b2 = pkg.row_band_for_slab(geom, W, H, zz0, zz1, mats)
+
             def st2():
                 v2.zero_()
-                pkg.pack_device(imgs, packed, stream)
-                pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream)
+                pkg.pack_device_band(imgs, b2, packed, err, stream)
+                pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream,
+                                       band=b2)
             for _ in range(2):
                 st2()
             if dist:
