@@ -230,6 +230,50 @@ def run_reference_arm(args):
 # our arm
 # ---------------------------------------------------------------------------------
 
+def calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world, args,
+                    rebalance_slabs, rounds=2):
+    """Times this rank's pack + back-projection step on its slab (untimed
+    warm-up work), gathers the times of all ranks and re-splits the planes
+    (rebalance_slabs) while max/mean > 1.02, at most `rounds` times."""
+    import torch
+
+    n, H, W = imgs.shape
+    L = g.edge_voxels
+    nb_full = pkg.packed_layout(W, H)[2]
+    packed = torch.empty(n * nb_full, dtype=torch.uint8, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    opt = pkg.Options(batch=args.batch, mode=pkg.MODE_EXACT if args.mode == "exact"
+                      else pkg.MODE_FAST)
+    stream = torch.cuda.current_stream(dev)
+    history = []
+    for it in range(rounds + 1):
+        z0, z1 = slabs[rank]
+        band = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
+        vol = torch.zeros(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for rep in range(2):
+            if rep == 1:
+                a.record(stream)
+            pkg.pack_device_band(imgs, band, packed, err, stream)
+            pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream,
+                                   band=band)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        times = [float(x.item()) for x in allt]
+        imb = max(times) / (sum(times) / world)
+        history.append(round(imb, 4))
+        del vol
+        if imb < 1.02 or it == rounds:
+            break
+        slabs = rebalance_slabs(work, slabs, times)
+    del packed
+    torch.cuda.empty_cache()
+    return {"slabs": [list(s) for s in slabs], "imbalance": history, "rounds": len(history) - 1}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -254,10 +298,17 @@ def run_ours(args):
     L = g.edge_voxels
     n, H, W = imgs.shape
     n_proj = n
+    balance = None
     if world > 1:
-        # z-slabs balanced by estimated (non-culled) work per plane, SURVEY H5
-        from paper_1401_3615_b200.distributed import balanced_slabs, plane_work
-        slabs = balanced_slabs(plane_work(g, mats, W, H), world)
+        # z-slabs balanced by estimated (non-culled) work per plane, SURVEY H5,
+        # then refined from each rank's measured step time (untimed warm-up)
+        from paper_1401_3615_b200.distributed import (balanced_slabs, plane_work,
+                                                      rebalance_slabs)
+        work = plane_work(g, mats, W, H)
+        slabs = balanced_slabs(work, world)
+        balance = calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world,
+                                  args, rebalance_slabs)
+        slabs = [tuple(s) for s in balance["slabs"]]
     else:
         slabs = [(0, L)]
     z0, z1 = slabs[rank]
@@ -365,6 +416,8 @@ def run_ours(args):
                    "projections": n, "detector": [W, H], "mode": args.mode,
                    "batch": args.batch, "parallelism": f"z-slab x{world}",
                    "slabs": [list(s) for s in slabs],
+                   "slab_balance": None if balance is None else {
+                       k: balance[k] for k in ("imbalance", "rounds")},
                    "row_band": {"rows": [band.raw_row0, band.raw_row0 + band.raw_rows],
                                 "cell_rows": band.cell_rows},
                    "l2": (f"inputs larger than L2 ({imgs.numel() * 4 / 1e9:.1f} GB raw + "

@@ -69,6 +69,20 @@ def balanced_slabs(work: np.ndarray, world: int) -> List[tuple]:
     return list(zip(bounds[:-1], bounds[1:]))
 
 
+def rebalance_slabs(work: np.ndarray, slabs: Sequence[tuple], seconds: Sequence[float]
+                    ) -> List[tuple]:
+    """One measured refinement of balanced_slabs: the estimated per-plane work
+    inside each slab is rescaled so that the slab's total equals its measured
+    time, then the planes are split again. Corrects what the sampled estimate
+    misses (culling granularity, per-launch overheads) without a cost model."""
+    w = np.asarray(work, dtype=np.float64).copy()
+    for (a, b), t in zip(slabs, seconds):
+        s = w[a:b].sum()
+        if b > a and s > 0 and t > 0:
+            w[a:b] *= float(t) / s
+    return balanced_slabs(w, len(slabs))
+
+
 def batch_roots(count: int, batch: int, world: int) -> List[tuple]:
     """(first, n, root) per batch: batch b is uploaded by rank b % world."""
     out = []
