@@ -119,6 +119,18 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry,
                            const cbb_options* options /* nullable */,
                            cbb_run_stats* stats /* nullable */);
 
+/* cbb_reconstruct for projections held in separate buffers, as the
+ * reference's ProjectionStack holds them (one std::vector<float> per
+ * ProjectionImage, proj/include/conebeam/dataset.hpp:15-60): imgs[i] points
+ * to height*width floats of projection i. Batches are gathered into pinned
+ * staging by several host threads while the GPU works on the previous batch,
+ * so no contiguous copy of the stack is needed. */
+cbb_status cbb_reconstruct_images(float* vol, const cbb_volume_geometry* geometry,
+                                  const float* const* imgs, int32_t width, int32_t height,
+                                  int32_t count, const double* mats,
+                                  const cbb_options* options /* nullable */,
+                                  cbb_run_stats* stats /* nullable */);
+
 /* ---- streaming from a CBPS stack file ------------------------------------ */
 
 /* Header of a CBPS stack file (proj/include/conebeam/dataset.hpp:62-72) --

@@ -58,16 +58,18 @@ inline void reconstruct(conebeam::Volume& vol, const conebeam::ProjectionStack& 
     if (vol.geometry != stack.geometry)
         throw conebeam::geometry_error("reconstruct_reference: volume and stack geometries differ");
     const int W = stack.images.front().width, H = stack.images.front().height;
-    const std::size_t pix = static_cast<std::size_t>(W) * H;
-    std::vector<float> imgs(pix * stack.count());
+    // the images stay where they are (one buffer each); only the 96-byte
+    // matrices are gathered
+    std::vector<const float*> imgs(stack.count());
     std::vector<double> mats(12 * stack.count());
     for (std::size_t i = 0; i < stack.count(); ++i) {
-        std::copy(stack.images[i].data.begin(), stack.images[i].data.end(), imgs.begin() + pix * i);
+        imgs[i] = stack.images[i].data.data();
         std::copy(stack.matrices[i].a.begin(), stack.matrices[i].a.end(), mats.begin() + 12 * i);
     }
     const cbb_volume_geometry g = to_c(vol.geometry);
-    throw_on(cbb_reconstruct(vol.voxels.data(), &g, imgs.data(), W, H,
-                             static_cast<int32_t>(stack.count()), mats.data(), options, stats));
+    throw_on(cbb_reconstruct_images(vol.voxels.data(), &g, imgs.data(), W, H,
+                                    static_cast<int32_t>(stack.count()), mats.data(), options,
+                                    stats));
 }
 
 } // namespace conebeam_b200

@@ -23,7 +23,7 @@ EXPORTS = (
     "cbb_backproject_device", "cbb_launch_count", "cbb_ramp_filter_device",
     "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
     "cbb_backproject_texture_device", "cbb_row_band_for_slab", "cbb_pack_device_band",
-    "cbb_backproject_device_band", "cbb_check_finite_device",
+    "cbb_backproject_device_band", "cbb_check_finite_device", "cbb_reconstruct_images",
 )
 
 
@@ -99,6 +99,10 @@ def _declare(L) -> None:
     L.cbb_reconstruct.restype = C.c_int
     L.cbb_reconstruct.argtypes = [_VP, C.POINTER(VolumeGeometryC), _VP, C.c_int32, C.c_int32,
                                   C.c_int32, _VP, C.POINTER(OptionsC), C.POINTER(RunStatsC)]
+    L.cbb_reconstruct_images.restype = C.c_int
+    L.cbb_reconstruct_images.argtypes = [_VP, C.POINTER(VolumeGeometryC), _VP, C.c_int32,
+                                         C.c_int32, C.c_int32, _VP, C.POINTER(OptionsC),
+                                         C.POINTER(RunStatsC)]
     L.cbb_session_create.restype = C.c_int
     L.cbb_session_create.argtypes = [C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32, _VP,
                                      C.POINTER(OptionsC), C.POINTER(_VP)]

@@ -148,6 +148,32 @@ def reconstruct_arrays(voxels: np.ndarray, geometry: VolumeGeometry, images: np.
     return st.to_dict()
 
 
+def reconstruct_images(voxels: np.ndarray, geometry: VolumeGeometry, images: Sequence,
+                       matrices: np.ndarray, options: Optional[Options] = None) -> dict:
+    """cbb_reconstruct_images: like reconstruct_arrays, but each projection is
+    its own (H, W) float32 array (the reference's one-buffer-per-image stack);
+    nothing is concatenated on the host."""
+    if voxels.dtype != np.float32 or not voxels.flags.c_contiguous:
+        raise ValidationError("voxels must be C-contiguous float32")
+    imgs = list(images)
+    if not imgs:
+        raise ValidationError("ProjectionStack: at least one projection required")
+    h, w = imgs[0].shape
+    for a in imgs:
+        if a.dtype != np.float32 or not a.flags.c_contiguous or a.shape != (h, w):
+            raise ValidationError("images must be C-contiguous float32 (H, W) arrays of one shape")
+    m = validate_matrices(matrices)
+    if m.shape[0] != len(imgs):
+        raise ValidationError("one matrix per image required")
+    ptrs = (C.c_void_p * len(imgs))(*[a.ctypes.data for a in imgs])
+    oc, _keep = (options or Options()).to_c()
+    st = _lib.RunStatsC()
+    _lib.check(_lib.lib().cbb_reconstruct_images(voxels.ctypes.data, C.byref(geometry_c(geometry)),
+                                                 ptrs, w, h, len(imgs), _ptr(m), C.byref(oc),
+                                                 C.byref(st)))
+    return st.to_dict()
+
+
 def stack_file_info(path: str) -> dict:
     """Header of a CBPS stack file (cbb_stack_file_query); raises IOError_,
     FormatError, TruncatedError like read_stack (proj/src/dataset.cpp:181-212)."""

@@ -48,3 +48,21 @@ for tag in ["plain"] + fracs:
         ref = vol.copy()
     else:
         print(f"  bitwise equal to plain: {np.array_equal(ref.view(np.uint32), vol.view(np.uint32))}")
+
+# the reference's stack layout: one pageable buffer per projection
+# (cbb_reconstruct_images), and one contiguous pageable array (cbb_reconstruct)
+os.environ.pop("CBB_NO_RESIDENT", None)
+os.environ.pop("CBB_TAIL_FRAC", None)
+parts = [np.array(imgs_h[i], copy=True) for i in range(len(imgs_h))]
+pageable = np.array(imgs_h, copy=True)
+for tag, fn in (("per-image buffers", lambda: pkg.reconstruct_images(vol, g, parts, mats, opt)),
+                ("contiguous pageable", lambda: pkg.reconstruct_arrays(vol, g, pageable, mats, opt))):
+    best = 1e9
+    for i in range(3):
+        vol[:] = 0
+        t0 = time.perf_counter()
+        st = fn()
+        best = min(best, time.perf_counter() - t0)
+    print(f"== {tag}: best {best * 1e3:.1f} ms -> {cfg.voxel_updates / best / 1e9:.1f} GUp/s "
+          f"(kernel {st['kernel_seconds'] * 1e3:.1f} ms)")
+    print(f"  bitwise equal to plain: {np.array_equal(ref.view(np.uint32), vol.view(np.uint32))}")

@@ -310,6 +310,24 @@ def test_nan_in_rows_no_band_holds_is_rejected(cuda, ids):
     assert np.all(vol.voxels == 2.0)
 
 
+@pytest.mark.parametrize("ids", [[0], [0, 0, 0]])
+def test_reconstruct_images_separate_buffers(cuda, ids):
+    """cbb_reconstruct_images (one buffer per projection, as the reference's
+    ProjectionStack holds them): bitwise the reference fixture; a null image
+    pointer or a NaN pixel is rejected and leaves the volume untouched."""
+    g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
+    parts = [np.array(imgs[i], copy=True) for i in range(len(imgs))]
+    v = vol0.copy()
+    st = pkg.reconstruct_images(v, g, parts, mats, pkg.Options(device_ids=ids, batch=4))
+    assert bits_equal(v, expected)
+    assert st["voxel_updates"] == g.edge_voxels ** 3 * len(mats)
+    parts[len(parts) // 2][1, 2] = np.nan
+    v2 = vol0.copy()
+    with pytest.raises(pkg.ValidationError):
+        pkg.reconstruct_images(v2, g, parts, mats, pkg.Options(device_ids=ids))
+    assert bits_equal(v2, vol0)
+
+
 @pytest.mark.parametrize("resident", [True, False])
 def test_w_zero_inside_slab_leaves_volume(cuda, monkeypatch, resident):
     """w == 0 exactly on plane z = 20 of a 32^3 volume (w = world z): the
