@@ -28,6 +28,7 @@
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -489,7 +490,7 @@ class DevicePool {
 
 // Pinned host staging cache: cudaHostAlloc pins pages at ~4 GB/s (measured:
 // 2 GiB in 565 ms), which for two 153 MB staging slots would cost ~80 ms per
-// cbb_reconstruct call; blocks are kept for the next call (at most 4, reused
+// cbb_reconstruct call; blocks are kept for the next call (at most 6, reused
 // when at least the request and at most twice its size).
 class HostPool {
   public:
@@ -523,7 +524,7 @@ class HostPool {
             return;
         free_.emplace(it->second, p);
         sizes_.erase(it);
-        while (free_.size() > 4) { // drop the smallest
+        while (free_.size() > 6) { // drop the smallest
             cudaFreeHost(free_.begin()->second);
             free_.erase(free_.begin());
         }
@@ -552,6 +553,7 @@ struct Worker {
     double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
     uint64_t guarded = 0;
     bool started = false;
+    bool k_end_set = false; // k_end already recorded (resident tail)
     // resident mode: every packed projection stays on the device; the head
     // planes [z_begin, tail_lo) + [tail_hi, z_end) are updated while the
     // batches stream in, the tail [tail_lo, tail_hi) afterwards while the
@@ -563,6 +565,7 @@ struct Worker {
     RowBand band;
     size_t pk_bytes = 0;               // packed bytes per projection (band rows)
     cudaEvent_t src_ready[2] = {};     // as root: raw slot filtered, peers may copy
+    cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
 
     ~Worker() {
         if (!copy)
@@ -578,6 +581,7 @@ struct Worker {
             cudaEventDestroy(h2d_done[i]);
             cudaEventDestroy(raw_free[i]);
             cudaEventDestroy(src_ready[i]);
+            cudaEventDestroy(xfer_ev[i]);
         }
         pool.release(device, d_err);
         pool.release(device, d_packed_all);
@@ -619,6 +623,79 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
         th.join();
 }
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// Host <-> device copies of large blocks for pageable host memory: a plain
+// cudaMemcpyAsync from/to pageable memory is synchronous and staged by the
+// driver at a fraction of the link rate. Here 64 MB chunks go through two
+// pinned buffers, the host copies (parallel_memcpy) overlapping the DMA of
+// the neighbouring chunk. Pinned memory is copied directly (asynchronously).
+// ev: two events of the stream's device.
+struct ChunkedXfer {
+    static constexpr size_t kChunk = size_t(64) << 20;
+    float* buf[2] = {nullptr, nullptr};
+    ~ChunkedXfer() {
+        for (auto b : buf)
+            HostPool::get().release(b);
+    }
+    void ensure() {
+        for (auto& b : buf)
+            if (!b)
+                b = HostPool::get().alloc(kChunk);
+    }
+    // returns after the last chunk left the pageable source
+    void upload(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
+        if (bytes == 0)
+            return;
+        if (is_pinned(src)) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+            return;
+        }
+        ensure();
+        int k = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
+            const size_t len = std::min(kChunk, bytes - off);
+            CK(cudaEventSynchronize(ev[k])); // buf[k]'s previous DMA finished
+            parallel_memcpy(buf[k], static_cast<const char*>(src) + off, len);
+            CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf[k], len,
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(ev[k], st));
+        }
+    }
+    // pageable dst: blocks until all bytes arrived; pinned dst: asynchronous
+    void download(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
+        if (bytes == 0)
+            return;
+        if (is_pinned(dst)) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+            return;
+        }
+        ensure();
+        const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+        auto issue = [&](size_t c) {
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            CK(cudaMemcpyAsync(buf[c & 1], static_cast<const char*>(src) + off, len,
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(ev[c & 1], st));
+        };
+        issue(0);
+        for (size_t c = 0; c < nchunks; ++c) {
+            if (c + 1 < nchunks)
+                issue(c + 1);
+            CK(cudaEventSynchronize(ev[c & 1]));
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            parallel_memcpy(static_cast<char*>(dst) + off, buf[c & 1], len);
+        }
+    }
+};
+
 double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.0f;
     CK(cudaEventElapsedTime(&ms, a, b));
@@ -631,6 +708,7 @@ struct Pipeline {
     cbb_options opt{};
     std::vector<std::unique_ptr<Worker>> workers;
     float* h_stage[2] = {nullptr, nullptr}; // pinned staging (batch x H x W)
+    ChunkedXfer xfer;                       // volume up/download for pageable buffers
     int stage_fill = 0;                     // projections staged in the current slot
     int slot = 0;                           // current staging / ring slot
     std::vector<double> stage_mats;         // matrices of the staged batch
@@ -796,6 +874,7 @@ struct Pipeline {
                 CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->src_ready[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->xfer_ev[s], cudaEventDisableTiming));
                 w->d_raw[s] = static_cast<float*>(
                     DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
                 w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
@@ -813,8 +892,8 @@ struct Pipeline {
             CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
             CK(cudaEventRecord(w->c_beg, w->copy));
             if (initial_volume && !opt.volume_is_zero)
-                CK(cudaMemcpyAsync(w->d_vol, initial_volume + plane * w->z_begin,
-                                   slab * sizeof(float), cudaMemcpyHostToDevice, w->copy));
+                xfer.upload(w->d_vol, initial_volume + plane * w->z_begin, slab * sizeof(float),
+                            w->copy, w->xfer_ev);
             else
                 CK(cudaMemsetAsync(w->d_vol, 0, slab * sizeof(float), w->copy));
             CK(cudaEventRecord(w->c_end, w->copy));
@@ -1097,9 +1176,38 @@ struct Pipeline {
         std::vector<double> mats(12 * (size_t)opt.batch);
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const int nt = (int)std::min<unsigned>(8, hw);
+        // the records are copied out of a read-only mapping of the file
+        // (page-cache pages mapped, no per-call kernel copy); pread when the
+        // file cannot be mapped
+        const uint64_t file_bytes = header_bytes + rec_bytes * (uint64_t)count;
+        const char* map = nullptr;
+        if (!std::getenv("CBB_FILE_PREAD")) {
+            void* m = ::mmap(nullptr, file_bytes, PROT_READ, MAP_SHARED, fd, 0);
+            if (m != MAP_FAILED) {
+                map = static_cast<const char*>(m);
+                ::madvise(m, file_bytes, MADV_SEQUENTIAL);
+            }
+        }
+        struct Unmap {
+            const char* p;
+            uint64_t n;
+            ~Unmap() {
+                if (p)
+                    ::munmap(const_cast<char*>(p), n);
+            }
+        } unmap{map, file_bytes};
+        double t_wait = 0, t_read = 0, t_issue = 0;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms_since = [](std::chrono::steady_clock::time_point t) {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t)
+                .count();
+        };
         for (int first = 0, n = 0; first < count; first += n) {
             n = batch_at(first, count);
+            auto t0 = now();
             wait_slot(slot);
+            t_wait += ms_since(t0);
+            t0 = now();
             float* dst = h_stage[slot];
             std::vector<std::thread> pool;
             std::vector<int> bad(nt, 0);
@@ -1107,9 +1215,14 @@ struct Pipeline {
                 pool.emplace_back([&, t] {
                     for (int j = t; j < n; j += nt) {
                         const uint64_t off = header_bytes + rec_bytes * (uint64_t)(first + j);
-                        if (!pread_all(fd, mats.data() + 12 * (size_t)j, 96, off) ||
-                            !pread_all(fd, dst + (size_t)j * W * H, rec_bytes - 96, off + 96))
+                        if (map) {
+                            std::memcpy(mats.data() + 12 * (size_t)j, map + off, 96);
+                            std::memcpy(dst + (size_t)j * W * H, map + off + 96, rec_bytes - 96);
+                        } else if (!pread_all(fd, mats.data() + 12 * (size_t)j, 96, off) ||
+                                   !pread_all(fd, dst + (size_t)j * W * H, rec_bytes - 96,
+                                              off + 96)) {
                             bad[t] = 1;
+                        }
                     }
                 });
             for (auto& th : pool)
@@ -1118,8 +1231,14 @@ struct Pipeline {
                 if (b)
                     fail(CBB_ERR_TRUNCATED, "file ends inside projection intensities");
             validate_matrices(mats.data(), n);
+            t_read += ms_since(t0);
+            t0 = now();
             issue(dst, mats.data(), n);
+            t_issue += ms_since(t0);
         }
+        if (std::getenv("CBB_TRACE"))
+            std::fprintf(stderr, "cbb: file stream: wait %.1f ms, read %.1f ms, issue %.1f ms\n",
+                         t_wait, t_read, t_issue);
     }
 
     static bool pread_all(int fd, void* buf, uint64_t bytes, uint64_t off) {
@@ -1142,8 +1261,9 @@ struct Pipeline {
         int err_any = 0;
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
-            if (close_timing && w->started)
+            if (close_timing && w->started && !w->k_end_set)
                 CK(cudaEventRecord(w->k_end, w->compute));
+            w->k_end_set = false;
             CK(cudaStreamSynchronize(w->compute));
             if (close_timing && w->started) {
                 w->kernel_s += elapsed_s(w->k_beg, w->k_end);
@@ -1171,10 +1291,10 @@ struct Pipeline {
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             const size_t slab = plane * (w->z_end - w->z_begin);
-            CK(cudaEventRecord(w->c_beg, w->compute));
-            CK(cudaMemcpyAsync(vol_out + plane * w->z_begin, w->d_vol, slab * sizeof(float),
-                               cudaMemcpyDeviceToHost, w->compute));
-            CK(cudaEventRecord(w->c_end, w->compute));
+            CK(cudaEventRecord(w->c_beg, w->copy));
+            xfer.download(vol_out + plane * w->z_begin, w->d_vol, slab * sizeof(float), w->copy,
+                          w->xfer_ev);
+            CK(cudaEventRecord(w->c_end, w->copy));
         }
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
@@ -1199,9 +1319,8 @@ struct Pipeline {
         cudaEvent_t t_tail = nullptr;
         auto d2h = [&](Worker& w, int z0, int z1) {
             if (z1 > z0)
-                CK(cudaMemcpyAsync(vol_out + plane * z0, w.d_vol + plane * (z0 - w.z_begin),
-                                   plane * (z1 - z0) * sizeof(float), cudaMemcpyDeviceToHost,
-                                   w.copy));
+                xfer.download(vol_out + plane * z0, w.d_vol + plane * (z0 - w.z_begin),
+                              plane * (z1 - z0) * sizeof(float), w.copy, w.xfer_ev);
         };
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
@@ -1209,26 +1328,34 @@ struct Pipeline {
                 CK(cudaEventCreate(&t_tail));
                 CK(cudaEventRecord(t_tail, w->compute));
             }
-            if (!overlap) {
-                w->guarded += launch_backproject(
-                    w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
-                    w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
-                    w->compute, 0, 0, &w->band);
-                continue;
-            }
-            // head out now; the tail copied out as soon as it is computed (no
-            // error can arise in it: tail_is_safe)
-            CK(cudaEventRecord(w->c_beg, w->copy));
-            d2h(*w, w->z_begin, w->tail_lo);
-            d2h(*w, w->tail_hi, w->z_end);
-            CK(cudaEventRecord(w->head_done, w->copy));
-            launch_backproject(w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo,
-                               w->tail_hi, w->d_packed_all, W, H, resident_count,
-                               all_mats.data(), opt, w->d_err, w->compute, 0, 0, &w->band);
+            w->guarded += launch_backproject(
+                w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
+                w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
+                w->compute, 0, 0, &w->band);
             CK(cudaEventRecord(w->tail_done, w->compute));
-            CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
-            d2h(*w, w->tail_lo, w->tail_hi);
-            CK(cudaEventRecord(w->c_end, w->copy));
+            if (w->started) { // kernel time ends with the tail, not the downloads
+                CK(cudaEventRecord(w->k_end, w->compute));
+                w->k_end_set = true;
+            }
+        }
+        if (overlap) {
+            // the tail runs on the compute streams (launched above) while the
+            // head is copied out; then the tail (no error can arise in it:
+            // tail_is_safe). Downloads into pageable memory block this
+            // thread chunk by chunk, the tail kernels keep running.
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
+                CK(cudaEventRecord(w->c_beg, w->copy));
+                d2h(*w, w->z_begin, w->tail_lo);
+                d2h(*w, w->tail_hi, w->z_end);
+                CK(cudaEventRecord(w->head_done, w->copy));
+            }
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
+                CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
+                d2h(*w, w->tail_lo, w->tail_hi);
+                CK(cudaEventRecord(w->c_end, w->copy));
+            }
         }
         // closes the kernel timing; with overlap this only re-checks flags
         // that cannot be set (pack errors were checked above)

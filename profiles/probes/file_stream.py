@@ -23,4 +23,31 @@ for i in range(3):
     dt = time.perf_counter() - t0
     print(f"reconstruct_file run {i}: {dt:.3f} s -> {cfg.voxel_updates / dt / 1e9:.1f} GUp/s "
           f"(kernel {st['kernel_seconds']:.3f} s)")
+pass
+
+# raw read throughput of the same file (page cache), for comparison
+import concurrent.futures as cf  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+pkg.write_stack(path, pkg.ProjectionStack(g, mats, imgs.numpy()))
+size = os.path.getsize(path)
+buf = np.empty(size, np.uint8)
+for nt in (1, 4, 8, 16):
+    fd = os.open(path, os.O_RDONLY)
+    per = (size + nt - 1) // nt
+
+    def rd(t):
+        off = t * per
+        mv = memoryview(buf)[off:min(size, off + per)]
+        done = 0
+        while done < len(mv):
+            done += os.preadv(fd, [mv[done:]], off + done)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(nt) as ex:
+        list(ex.map(rd, range(nt)))
+    dt = time.perf_counter() - t0
+    os.close(fd)
+    print(f"raw pread {nt:2d} threads: {size / dt / 1e9:.1f} GB/s")
 os.remove(path)
