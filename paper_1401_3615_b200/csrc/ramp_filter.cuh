@@ -75,7 +75,11 @@ inline int rf_nfft(int W) {
 }
 
 // Cached per (device, nfft, rows, tau): plans, work buffers, spectrum of h.
+// The work buffers (and cuFFT's own work areas) are shared by every stream of
+// the device, so uses are chained on the GPU: each use waits for `last` (the
+// previous use, possibly on another stream) and records it when done.
 struct RampPlan {
+    cudaEvent_t last = nullptr;
     cufftHandle fwd = 0, inv = 0;
     double* pad = nullptr;
     double2* spec = nullptr;
@@ -120,6 +124,7 @@ class RampPlans {
             fail(CBB_ERR_INTERNAL, "cufftExecD2Z(h) failed");
         check_cuda(cudaStreamSynchronize(st), "ramp spectrum");
         cufftDestroy(one);
+        check_cuda(cudaEventCreateWithFlags(&p.last, cudaEventDisableTiming), "ramp event");
         return plans_.emplace(key, p).first->second;
     }
     std::mutex mu;
@@ -141,6 +146,7 @@ inline void ramp_filter_device(const float* raw, float* out, int W, int H, int c
     RampPlan& p = pl.plan(dev, W, kRampRows, tau, st);
     cufftSetStream(p.fwd, st);
     cufftSetStream(p.inv, st);
+    check_cuda(cudaStreamWaitEvent(st, p.last, 0), "ramp: wait previous use");
     const int nc = p.nfft / 2 + 1;
     for (long long r0 = 0; r0 < rows_total; r0 += kRampRows) {
         const long long rows = std::min(kRampRows, rows_total - r0);
@@ -161,6 +167,7 @@ inline void ramp_filter_device(const float* raw, float* out, int W, int H, int c
         check_cuda(cudaGetLastError(), "ramp filter kernels");
         g_launches += 3;
     }
+    check_cuda(cudaEventRecord(p.last, st), "ramp: record use");
 }
 
 } // namespace cbb

@@ -260,7 +260,8 @@ def _bands_from_trace(err: str):
     return out
 
 
-@pytest.mark.parametrize("ids,filt", [([0, 0, 0, 0], False), ([0, 0, 0], True)])
+@pytest.mark.parametrize("ids,filt", [([0, 0, 0, 0], False), ([0, 0, 0], True),
+                                      ([0, 0, 0, 0, 0], True)])
 def test_row_bands_and_rotating_roots_bitwise(cuda, oracle, monkeypatch, capfd, ids, filt):
     """Several slab workers: batch k is uploaded once by worker k mod G and the
     others copy only the detector rows their slab projects onto (strided peer
