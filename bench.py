@@ -563,7 +563,15 @@ def run_ours(args):
                        "d2h_bytes_per_step": int((z1 - z0) * L * L * 4),
                        "seconds": round(e2e_t, 4), "path": path,
                        "phases": {k: round(v, 4) if isinstance(v, float) else v
-                                  for k, v in stats.items() if k != "per_gpu_kernel_seconds"}}
+                                  for k, v in stats.items()
+                                  if k not in ("per_gpu_kernel_seconds", "culled_updates",
+                                               "culled_fraction")}}
+        if world == 1:
+            # one untimed call with the culling counters on (slower kernels)
+            cst = pkg.reconstruct_arrays(buf, g, imgs_np, mats, pkg.Options(
+                batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
+                volume_is_zero=True, count_culled=True))
+            line["culled_fraction"] = round(cst["culled_fraction"], 4)
         del vol_h
 
     # CPU baseline: the reference's CPU path on this box's host cores (rank 0, N=1)

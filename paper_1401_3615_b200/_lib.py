@@ -47,14 +47,15 @@ class OptionsC(C.Structure):
                 ("batch", C.c_int32), ("mode", C.c_int32), ("cull", C.c_int32),
                 ("volume_is_zero", C.c_int32), ("slab_begin", C.c_int32),
                 ("slab_end", C.c_int32), ("ramp_filter", C.c_int32),
-                ("filter_pixel_mm", C.c_double)]
+                ("filter_pixel_mm", C.c_double), ("count_culled", C.c_int32)]
 
 
 class RunStatsC(C.Structure):
     _fields_ = [("total_seconds", C.c_double), ("h2d_seconds", C.c_double),
                 ("kernel_seconds", C.c_double), ("d2h_seconds", C.c_double),
                 ("voxel_updates", C.c_uint64), ("guarded_batches", C.c_uint64),
-                ("num_gpus", C.c_int32), ("per_gpu_kernel_seconds", C.c_double * 8)]
+                ("num_gpus", C.c_int32), ("per_gpu_kernel_seconds", C.c_double * 8),
+                ("culled_updates", C.c_uint64), ("culled_fraction", C.c_double)]
 
     def to_dict(self) -> dict:
         return {
@@ -63,6 +64,8 @@ class RunStatsC(C.Structure):
             "voxel_updates": int(self.voxel_updates),
             "guarded_batches": int(self.guarded_batches), "num_gpus": int(self.num_gpus),
             "per_gpu_kernel_seconds": list(self.per_gpu_kernel_seconds)[: max(self.num_gpus, 0)],
+            "culled_updates": int(self.culled_updates),
+            "culled_fraction": self.culled_fraction,
         }
 
 

@@ -45,6 +45,7 @@ class Options:
     volume_is_zero: bool = False
     slab: Optional[Sequence[int]] = None  # (z_begin, z_end) planes to update; None = all
     ramp_filter_pixel_mm: Optional[float] = None  # set: inputs are raw line integrals, FDK-filter on GPU
+    count_culled: bool = False        # run stats report culled updates (slower kernels)
 
     def to_c(self):
         o = _lib.OptionsC()
@@ -65,6 +66,7 @@ class Options:
         if self.ramp_filter_pixel_mm is not None:
             o.ramp_filter = 1
             o.filter_pixel_mm = float(self.ramp_filter_pixel_mm)
+        o.count_culled = int(bool(self.count_culled))
         return o, keep
 
 

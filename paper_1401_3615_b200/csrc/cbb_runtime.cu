@@ -311,7 +311,7 @@ void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st)
     ++g_launches;
 }
 
-template <int R, int MODE, bool GUARD, int MINB, int SW = 0>
+template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false>
 void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
@@ -324,7 +324,7 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
                              ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
         grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
     }
-    bp_kernel<R, MODE, GUARD, MINB, SW><<<grid, block, 0, st>>>(args, mats);
+    bp_kernel<R, MODE, GUARD, MINB, SW, CNT><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -339,8 +339,10 @@ int bp_variant() {
 
 template <int MODE, bool GUARD>
 void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
-    if (GUARD)
+    if (GUARD) // (culling does not run in the guarded kernel: nothing to count)
         return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
+    if (args.counters) // statistics requested: the counting instantiation
+        return launch_bp_r<8, MODE, GUARD, 3, 0, true>(args, mats, nz, st);
     switch (bp_variant()) {
     case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
     case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
@@ -355,7 +357,8 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
                             int z_end, const void* packed, int W, int H, int count,
                             const double* mats, const cbb_options& opt, int* err,
                             cudaStream_t st, int gap_lo = 0, int gap_hi = 0,
-                            const RowBand* band = nullptr) {
+                            const RowBand* band = nullptr,
+                            unsigned long long* counters = nullptr) {
     const int qp = quad_pitch_cells(W);
     const RowBand b = band ? *band : RowBand::full(H);
     // packed projections of qn rows each; cell row q0 is the buffer's first
@@ -374,6 +377,7 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.qpitchf = (float)qp;
     args.cell_bias = (float)(kPad * qp + kPad) + 8388608.0f;
     args.err = err;
+    args.counters = counters;
     args.neg_zero2 = 0x8000000080000000ull;
     args.cull = opt.cull ? 1 : 0;
     // optional skipped planes [gap_lo, gap_hi) (absolute z, gap_lo - z_begin
@@ -566,6 +570,8 @@ struct Worker {
     size_t pk_bytes = 0;               // packed bytes per projection (band rows)
     cudaEvent_t src_ready[2] = {};     // as root: raw slot filtered, peers may copy
     cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
+    unsigned long long* d_counters = nullptr; // kCounterSlots culled-update counters
+    bool count_culled = false;
 
     ~Worker() {
         if (!copy)
@@ -584,6 +590,7 @@ struct Worker {
             cudaEventDestroy(xfer_ev[i]);
         }
         pool.release(device, d_err);
+        pool.release(device, d_counters);
         pool.release(device, d_packed_all);
         if (head_done)
             cudaEventDestroy(head_done);
@@ -890,6 +897,11 @@ struct Pipeline {
                 DevicePool::get().alloc(w->device, std::max<size_t>(slab, 1) * sizeof(float)));
             w->d_err = static_cast<int*>(DevicePool::get().alloc(w->device, sizeof(int)));
             CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
+            const size_t cbytes = sizeof(unsigned long long) * kCounterSlots;
+            w->d_counters = static_cast<unsigned long long*>(
+                DevicePool::get().alloc(w->device, cbytes));
+            CK(cudaMemsetAsync(w->d_counters, 0, cbytes, w->compute));
+            w->count_culled = opt.count_culled != 0;
             CK(cudaEventRecord(w->c_beg, w->copy));
             if (initial_volume && !opt.volume_is_zero)
                 xfer.upload(w->d_vol, initial_volume + plane * w->z_begin, slab * sizeof(float),
@@ -990,7 +1002,7 @@ struct Pipeline {
             w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end, packed, W, H, n,
                                              mats, opt, w->d_err, w->compute,
                                              resident ? w->tail_lo : 0, resident ? w->tail_hi : 0,
-                                             &w->band);
+                                             &w->band, w->count_culled ? w->d_counters : nullptr);
         }
         ++nbatch;
         if (resident)
@@ -1331,7 +1343,7 @@ struct Pipeline {
             w->guarded += launch_backproject(
                 w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
                 w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
-                w->compute, 0, 0, &w->band);
+                w->compute, 0, 0, &w->band, w->count_culled ? w->d_counters : nullptr);
             CK(cudaEventRecord(w->tail_done, w->compute));
             if (w->started) { // kernel time ends with the tail, not the downloads
                 CK(cudaEventRecord(w->k_end, w->compute));
@@ -1386,10 +1398,20 @@ struct Pipeline {
         resident = false;
     }
 
-    void fill_stats(cbb_run_stats* st, double total) const {
+    void fill_stats(cbb_run_stats* st, double total) {
         if (!st)
             return;
         std::memset(st, 0, sizeof *st);
+        uint64_t culled = 0;
+        for (auto& w : workers) {
+            std::vector<unsigned long long> c(kCounterSlots);
+            CK(cudaSetDevice(w->device));
+            CK(cudaMemcpy(c.data(), w->d_counters, sizeof(unsigned long long) * c.size(),
+                          cudaMemcpyDeviceToHost));
+            for (auto x : c)
+                culled += x;
+        }
+        st->culled_updates = culled;
         st->total_seconds = total;
         st->num_gpus = (int32_t)workers.size();
         uint64_t planes = 0;
@@ -1405,6 +1427,10 @@ struct Pipeline {
             if (i < 8)
                 st->per_gpu_kernel_seconds[i] = w.kernel_s;
         }
+        st->culled_fraction = !opt.count_culled ? -1.0
+                              : st->voxel_updates
+                                  ? (double)st->culled_updates / (double)st->voxel_updates
+                                  : 0.0;
     }
 };
 
@@ -1461,6 +1487,7 @@ void cbb_options_defaults(cbb_options* o) {
     o->slab_end = 0;
     o->ramp_filter = 0;
     o->filter_pixel_mm = 0.0;
+    o->count_culled = 0;
 }
 
 cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int32_t* qrows,

@@ -311,6 +311,37 @@ def test_nan_in_rows_no_band_holds_is_rejected(cuda, ids):
     assert np.all(vol.voxels == 2.0)
 
 
+def test_culled_update_counters(cuda):
+    """cbb_run_stats.culled_updates: (voxel, projection) pairs skipped by warp
+    culling. Never more than the pairs whose position is off the detector
+    (ix <= -2, ix >= W, iy <= -2 or iy >= H, counted here in float64), most
+    of them (> 25 % here) when the volume overhangs the field of view, and 0 with culling
+    off; the volume is bitwise the same either way."""
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=24)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=12)
+    imgs = imgs_t.numpy()
+    L = g.edge_voxels
+    zero = np.zeros((L,) * 3, np.float32)
+    v_on, st_on = gpu_reconstruct(g, mats, imgs, zero, cull=True, device_ids=[0, 0],
+                                  count_culled=True)
+    v_off, st_off = gpu_reconstruct(g, mats, imgs, zero, cull=False, count_culled=True)
+    v_nc, st_nc = gpu_reconstruct(g, mats, imgs, zero)
+    assert bits_equal(v_on, v_off) and bits_equal(v_on, v_nc)
+    assert st_off["culled_updates"] == 0 and st_off["culled_fraction"] == 0.0
+    assert st_nc["culled_fraction"] == -1.0
+    idx = g.origin_mm + np.arange(L) * g.voxel_mm
+    Z, Y, X = np.meshgrid(idx, idx, idx, indexing="ij")
+    hom = np.stack([X.ravel(), Y.ravel(), Z.ravel(), np.ones(X.size)])
+    off = 0
+    for a in mats:
+        u, v, w = a.reshape(4, 3).T @ hom
+        ix, iy = u / w, v / w
+        off += int(np.count_nonzero((ix <= -2) | (ix >= cfg.width) | (iy <= -2) | (iy >= cfg.height)))
+    assert 0 < st_on["culled_updates"] <= off
+    assert st_on["culled_updates"] > 0.25 * off, (st_on["culled_updates"], off)
+    assert st_on["culled_fraction"] == pytest.approx(st_on["culled_updates"] / st_on["voxel_updates"])
+
+
 @pytest.mark.parametrize("ids", [[0], [0, 0, 0]])
 def test_reconstruct_images_separate_buffers(cuda, ids):
     """cbb_reconstruct_images (one buffer per projection, as the reference's

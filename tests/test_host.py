@@ -189,8 +189,8 @@ def test_struct_layouts_match_header():
     from paper_1401_3615_b200 import _lib
 
     assert ctypes.sizeof(_lib.VolumeGeometryC) == 24
-    assert ctypes.sizeof(_lib.OptionsC) == 56
-    assert ctypes.sizeof(_lib.RunStatsC) == 8 * 4 + 8 * 2 + 8 + 8 * 8
+    assert ctypes.sizeof(_lib.OptionsC) == 64
+    assert ctypes.sizeof(_lib.RunStatsC) == 8 * 4 + 8 * 2 + 8 + 8 * 8 + 8 + 8
     assert ctypes.sizeof(_lib.StackFileInfoC) == 40
 
 
