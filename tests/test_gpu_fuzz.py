@@ -1,0 +1,88 @@
+"""Seeded fuzz of the whole host pipeline against the oracle (bitwise):
+random circular scans (source distance, magnification, detector size and
+pitch, angular range, volume size and voxel size, volume offset from the
+isocentre so the detector is over- or under-filled), random batch sizes,
+1-4 slab workers sharing the GPU (rotating upload roots, row bands, peer band
+copies), resident tail on or off, random initial volumes with -0.0 voxels,
+contiguous / per-image / pageable / file inputs. A few cases use random
+matrices (w changes sign -> guarded kernel, possibly w == 0 -> GeometryError
+with the volume untouched)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+import paper_1401_3615_b200 as pkg
+from paper_1401_3615_b200.geometry import (TrajectoryConfig, VolumeGeometry,
+                                           make_circular_trajectory)
+
+pytestmark = pytest.mark.gpu
+
+
+def case(seed):
+    r = np.random.default_rng(seed)
+    L = int(r.integers(12, 49))
+    W = int(r.integers(6, 90))
+    H = int(r.integers(6, 70))
+    n = int(r.integers(1, 45))
+    voxel = float(r.uniform(0.3, 3.0))
+    sid = float(r.uniform(60.0, 400.0))
+    sdd = sid * float(r.uniform(1.1, 2.5))
+    # pixel pitch so that the detector covers 40 %-160 % of the volume
+    cover = float(r.uniform(0.4, 1.6))
+    pitch = cover * L * voxel * (sdd / sid) / max(W, H)
+    rng_deg = float(r.choice([180.0, 200.0, 360.0]))
+    cfg = TrajectoryConfig(n, sid, sdd, W, H, pitch, math.radians(rng_deg))
+    mats = make_circular_trajectory(cfg)
+    if seed % 7 == 3:  # random matrices: w changes sign over the volume
+        mats = r.standard_normal((n, 12))
+        mats[:, 11] += 2.0
+    origin = -0.5 * (L - 1) * voxel + float(r.uniform(-0.3, 0.3)) * L * voxel
+    g = VolumeGeometry(L, voxel, origin)
+    imgs = r.standard_normal((n, H, W)).astype(np.float32)
+    imgs[r.random((n, H, W)) < 0.2] = 0.0
+    vol0 = (r.standard_normal((L, L, L)) * float(r.choice([0.0, 1.0]))).astype(np.float32)
+    if r.random() < 0.3:
+        vol0[r.random(vol0.shape) < 0.1] = -0.0
+    k = int(r.integers(1, 5))
+    opts = dict(batch=int(r.integers(1, 33)), device_ids=[0] * k,
+                mode=pkg.MODE_EXACT, cull=bool(r.random() < 0.85))
+    return g, mats, imgs, vol0, opts, r
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("CBB_FUZZ_SEEDS", "24"))))
+def test_fuzz_pipeline_vs_oracle(cuda, oracle, monkeypatch, tmp_path, seed):
+    g, mats, imgs, vol0, opts, r = case(seed)
+    ref = vol0.copy()
+    status = oracle.reconstruct(ref, g, imgs, mats)
+    if r.random() < 0.5:
+        monkeypatch.setenv("CBB_NO_RESIDENT", "1")
+    how = ["contiguous", "images", "pageable", "file"][seed % 4]
+    v = vol0.copy()
+
+    def run():
+        if how == "contiguous":
+            vol = pkg.Volume(g, v)
+            return pkg.reconstruct(vol, pkg.ProjectionStack(g, mats, imgs), pkg.Options(**opts))
+        if how == "images":
+            return pkg.reconstruct_images(v, g, [np.array(a) for a in imgs], mats,
+                                          pkg.Options(**opts))
+        if how == "pageable":
+            return pkg.reconstruct_arrays(v, g, np.array(imgs), mats, pkg.Options(**opts))
+        p = str(tmp_path / f"s{seed}.cbps")
+        pkg.write_stack(p, pkg.ProjectionStack(g, mats, imgs))
+        out, st = pkg.reconstruct_file(p, pkg.Options(**opts), initial=pkg.Volume(g, v))
+        v[...] = out.voxels
+        return st
+
+    if status != 0:
+        assert status == 5
+        with pytest.raises(pkg.GeometryError):
+            run()
+        assert bits_equal(v, vol0)
+        return
+    run()
+    assert bits_equal(v, ref), (seed, how, opts)
