@@ -4,7 +4,8 @@ Drop-in for the reference's hot path (proj/src/kernel_ref.cpp:5-38,
 proj/src/kernel_opt.cpp:658-716) through the C ABI in include/conebeam_b200.h.
 """
 from .backproject import (MODE_EXACT, MODE_FAST, Options, RowBand, Session, backproject,
-                          backproject_device, check_finite_device, compare_volumes_device,
+                          backproject_device, backproject_texture_device, check_finite_device,
+                          compare_volumes_device,
                           device_count, launch_count, pack_device, pack_device_band,
                           packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays,
                           reconstruct_file, reconstruct_images, row_band_for_slab,
@@ -17,7 +18,7 @@ from .geometry import (TrajectoryConfig, VolumeGeometry, dehomogenize, forward_p
 
 __all__ = [
     "MODE_EXACT", "MODE_FAST", "Options", "RowBand", "Session", "backproject",
-    "backproject_device", "check_finite_device", "compare_volumes_device",
+    "backproject_device", "backproject_texture_device", "check_finite_device", "compare_volumes_device",
     "pack_device_band", "row_band_for_slab",
     "device_count", "launch_count", "pack_device", "packed_layout", "ramp_filter_device", "reconstruct",
     "reconstruct_arrays", "reconstruct_file", "reconstruct_images", "stack_file_info", "ProjectionStack", "Volume", "read_stack", "read_volume",

@@ -24,6 +24,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1563,11 +1564,32 @@ cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geom
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         const int L = geometry->edge_voxels;
         constexpr int kLayers = 2048; // layered-texture depth limit
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        // one layered array per device, kept between calls (allocating and
+        // freeing GB-sized arrays costs tens of ms)
+        static std::mutex arr_mu;
+        static std::map<int, std::tuple<cudaArray_t, int, int, int>> arrays;
+        std::lock_guard<std::mutex> lk(arr_mu);
         for (int chunk0 = 0; chunk0 < count; chunk0 += kLayers) {
             const int nc = std::min(kLayers, count - chunk0);
             cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
-            cudaArray_t arr = nullptr;
-            CK(cudaMalloc3DArray(&arr, &fd, make_cudaExtent(width, height, nc), cudaArrayLayered));
+            auto it = arrays.find(dev);
+            if (it != arrays.end() && (std::get<1>(it->second) != width ||
+                                       std::get<2>(it->second) != height ||
+                                       std::get<3>(it->second) < nc)) {
+                CK(cudaStreamSynchronize(st));
+                cudaFreeArray(std::get<0>(it->second));
+                arrays.erase(it);
+                it = arrays.end();
+            }
+            if (it == arrays.end()) {
+                cudaArray_t a = nullptr;
+                CK(cudaMalloc3DArray(&a, &fd, make_cudaExtent(width, height, nc),
+                                     cudaArrayLayered));
+                it = arrays.emplace(dev, std::make_tuple(a, width, height, nc)).first;
+            }
+            cudaArray_t arr = std::get<0>(it->second);
             cudaMemcpy3DParms cp = {};
             cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(raw) + (size_t)chunk0 * width * height,
                                             (size_t)width * sizeof(float), width, height);
@@ -1600,11 +1622,11 @@ cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geom
                 ++g_launches;
                 e = cudaGetLastError();
             }
-            // the array and texture are released once the chunk has run
+            // the texture object is released (and the array reused) once the
+            // chunk has run
             const cudaError_t es = cudaStreamSynchronize(st);
             if (tex)
                 cudaDestroyTextureObject(tex);
-            cudaFreeArray(arr);
             CK(e);
             CK(es);
         }

@@ -500,3 +500,27 @@ def test_config2_full_size_planes_bitwise(cuda, oracle):
         slab = np.zeros((1, L, L), np.float32)
         assert oracle.reconstruct_slab(slab, g, z0, z0 + 1, host, mats) == 0
         assert bits_equal(vol[z0:z0 + 1].cpu().numpy(), slab), f"plane {z0}"
+
+
+def test_texture_side_variant_is_close_not_exact(cuda, oracle):
+    """cbb_backproject_texture_device (north_star's hardware-texture side
+    number): 8-bit texture weights and floor addressing put it near, not at,
+    the reference -- relL2 0.05-0.15 (coarser grids err more), far above
+    the 1e-5 parity bar, so it is only ever reported beside the exact
+    result."""
+    import torch
+
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=48, num_projections=40)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=20)
+    imgs = imgs_t.numpy()
+    ref = np.zeros((48,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    vt = torch.zeros((48,) * 3, dtype=torch.float32, device="cuda")
+    raw = torch.from_numpy(imgs).cuda()
+    for _ in range(2):  # second call reuses the cached layered array
+        vt.zero_()
+        pkg.backproject_texture_device(vt, g, 0, 48, raw, mats)
+    torch.cuda.synchronize()
+    v = vt.cpu().numpy()
+    e = rel_l2(v, ref)
+    assert 1e-5 < e < 0.3, e
