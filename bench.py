@@ -510,6 +510,7 @@ def run_ours(args):
         del vt
         line["secondary"] = sec
         torch.cuda.empty_cache()
+        pkg.release_cached_memory()  # e.g. the texture variant's layered array
 
     # e2e through the public host API: pinned host projections -> host volume
     if not args.no_e2e:

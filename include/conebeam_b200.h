@@ -283,6 +283,11 @@ typedef struct cbb_volume_diff {
 cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64_t n,
                                       double denom_floor, cbb_volume_diff* out, void* stream);
 
+/* Frees the library's cached device buffers, pinned host staging and texture
+ * arrays (kept between calls to avoid allocation costs), like
+ * torch.cuda.empty_cache. Call when no other cbb_* call is running. */
+cbb_status cbb_release_cached_memory(void);
+
 /* Number of kernel launches the last cbb_backproject_device / cbb_pack_device
  * calls on this thread issued (for the bench's gpu_launches count). */
 uint64_t cbb_launch_count(void);

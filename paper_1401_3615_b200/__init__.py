@@ -8,7 +8,8 @@ from .backproject import (MODE_EXACT, MODE_FAST, Options, RowBand, Session, back
                           compare_volumes_device,
                           device_count, launch_count, pack_device, pack_device_band,
                           packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays,
-                          reconstruct_file, reconstruct_images, row_band_for_slab,
+                          reconstruct_file, reconstruct_images, release_cached_memory,
+                          row_band_for_slab,
                           stack_file_info)
 from .dataset import ProjectionStack, Volume, read_stack, read_volume, write_stack, write_volume
 from .errors import (ConebeamError, FormatError, GeometryError, InternalError, IOError_,
@@ -19,7 +20,7 @@ from .geometry import (TrajectoryConfig, VolumeGeometry, dehomogenize, forward_p
 __all__ = [
     "MODE_EXACT", "MODE_FAST", "Options", "RowBand", "Session", "backproject",
     "backproject_device", "backproject_texture_device", "check_finite_device", "compare_volumes_device",
-    "pack_device_band", "row_band_for_slab",
+    "pack_device_band", "release_cached_memory", "row_band_for_slab",
     "device_count", "launch_count", "pack_device", "packed_layout", "ramp_filter_device", "reconstruct",
     "reconstruct_arrays", "reconstruct_file", "reconstruct_images", "stack_file_info", "ProjectionStack", "Volume", "read_stack", "read_volume",
     "write_stack", "write_volume", "ConebeamError", "FormatError", "GeometryError",

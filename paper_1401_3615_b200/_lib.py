@@ -24,6 +24,7 @@ EXPORTS = (
     "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
     "cbb_backproject_texture_device", "cbb_row_band_for_slab", "cbb_pack_device_band",
     "cbb_backproject_device_band", "cbb_check_finite_device", "cbb_reconstruct_images",
+    "cbb_release_cached_memory",
 )
 
 
@@ -153,6 +154,8 @@ def _declare(L) -> None:
                                               _VP, _VP]
     L.cbb_check_finite_device.restype = C.c_int
     L.cbb_check_finite_device.argtypes = [_VP, C.c_int64, _VP, _VP]
+    L.cbb_release_cached_memory.restype = C.c_int
+    L.cbb_release_cached_memory.argtypes = []
     L.cbb_launch_count.restype = C.c_uint64
     L.cbb_launch_count.argtypes = []
 

@@ -261,6 +261,12 @@ class Session:
 
 # --- device-resident path (torch tensors as plain device memory) ---------------
 
+def release_cached_memory() -> None:
+    """Frees the library's cached device/pinned buffers and texture arrays
+    (cbb_release_cached_memory), like torch.cuda.empty_cache."""
+    _lib.check(_lib.lib().cbb_release_cached_memory())
+
+
 def packed_layout(width: int, height: int) -> tuple:
     """(quad_pitch, quad_rows, bytes_per_projection) of the packed gather layout."""
     qp, qr, nb = C.c_int32(), C.c_int32(), C.c_int64()

@@ -486,6 +486,21 @@ class DevicePool {
             cudaFree(kv.second);
         free_[device].clear();
     }
+    void trim_all() {
+        std::vector<int> devs;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto& kv : free_)
+                devs.push_back(kv.first);
+        }
+        for (int d : devs) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            trim(d);
+            cudaSetDevice(cur);
+        }
+    }
 
   private:
     std::mutex mu_;
@@ -533,6 +548,12 @@ class HostPool {
             cudaFreeHost(free_.begin()->second);
             free_.erase(free_.begin());
         }
+    }
+    void trim() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& kv : free_)
+            cudaFreeHost(kv.second);
+        free_.clear();
     }
 
   private:
@@ -1548,6 +1569,28 @@ cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64
     });
 }
 
+namespace {
+std::mutex g_tex_mu;
+std::map<int, std::tuple<cudaArray_t, int, int, int>> g_tex_arrays; // device -> array, W, H, layers
+} // namespace
+
+cbb_status cbb_release_cached_memory(void) {
+    return guarded([&] {
+        DevicePool::get().trim_all();
+        HostPool::get().trim();
+        std::lock_guard<std::mutex> lk(g_tex_mu);
+        for (auto& kv : g_tex_arrays) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(kv.first);
+            cudaDeviceSynchronize();
+            cudaFreeArray(std::get<0>(kv.second));
+            cudaSetDevice(cur);
+        }
+        g_tex_arrays.clear();
+    });
+}
+
 cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geometry* geometry,
                                           int32_t z_begin, int32_t z_end, const float* raw,
                                           int32_t width, int32_t height, int32_t count,
@@ -1568,9 +1611,8 @@ cbb_status cbb_backproject_texture_device(float* vol_slab, const cbb_volume_geom
         CK(cudaGetDevice(&dev));
         // one layered array per device, kept between calls (allocating and
         // freeing GB-sized arrays costs tens of ms)
-        static std::mutex arr_mu;
-        static std::map<int, std::tuple<cudaArray_t, int, int, int>> arrays;
-        std::lock_guard<std::mutex> lk(arr_mu);
+        auto& arrays = g_tex_arrays;
+        std::lock_guard<std::mutex> lk(g_tex_mu);
         for (int chunk0 = 0; chunk0 < count; chunk0 += kLayers) {
             const int nc = std::min(kLayers, count - chunk0);
             cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
