@@ -528,3 +528,45 @@ def test_texture_side_variant_is_close_not_exact(cuda, oracle):
     pkg.release_cached_memory()
     v2, _ = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref))
     assert bits_equal(v2, ref)
+
+
+@pytest.mark.slow
+def test_config0_and_config1_full_volumes_bitwise(cuda, oracle):
+    """BASELINE configs 0 (128^3) and 1 (256^3), all 496 projections, through
+    the host C ABI (pinned input, two slab workers for config 1): the whole
+    volume bitwise against the threaded oracle."""
+    for cid, ids in ((0, [0]), (1, [0, 0])):
+        cfg = synth.CONFIGS[cid]
+        g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=62)
+        imgs = imgs_t.numpy()
+        L = g.edge_voxels
+        ref = np.zeros((L,) * 3, np.float32)
+        assert oracle.reconstruct(ref, g, imgs, mats) == 0
+        v = np.zeros_like(ref)
+        st = pkg.reconstruct_arrays(v, g, imgs, mats, pkg.Options(device_ids=ids))
+        assert st["voxel_updates"] == L ** 3 * 496 and st["guarded_batches"] == 0
+        assert bits_equal(v, ref), f"config {cid}"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid,count", [(3, 496), (4, 180)])
+def test_1024_volumes_planes_bitwise(cuda, oracle, cid, count):
+    """The 1024^3 volumes (4 GiB): config 3 (496 x 1248x960) and config 4's
+    detector and trajectory (1536x1536, 360 deg; first 180 of its 1440
+    projections) through cbb_reconstruct into a pinned host volume with the
+    resident tail; the oracle recomputes the bottom, centre and top planes."""
+    import torch
+
+    cfg = synth.CONFIGS[cid]
+    g, mats, imgs = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=30,
+                                      count=count, pin=True)
+    L = g.edge_voxels
+    vol_t = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
+    v = vol_t.numpy()
+    st = pkg.reconstruct_arrays(v, g, imgs.numpy(), mats, pkg.Options(volume_is_zero=True))
+    assert st["voxel_updates"] == L ** 3 * count
+    host = imgs.numpy()
+    for z0 in (0, L // 2, L - 1):
+        slab = np.zeros((1, L, L), np.float32)
+        assert oracle.reconstruct_slab(slab, g, z0, z0 + 1, host, mats) == 0
+        assert bits_equal(v[z0:z0 + 1], slab), f"config {cid} plane {z0}"
