@@ -1,0 +1,247 @@
+// memory.cuh -- device / pinned-host buffer caches and host<->device
+// transfers of large pageable blocks.
+// Internal part of libconebeam_b200.so: included, in this order, by
+// cbb_runtime.cu (one translation unit: runtime_common.cuh, launch.cuh,
+// memory.cuh, pipeline.cuh).
+#pragma once
+
+namespace cbb {
+
+// ---------------------------------------------------------------------------
+// Device buffer cache: repeated reconstructions (per-projection calls,
+// benchmark loops) reuse device buffers instead of paying cudaMalloc/cudaFree
+// (~ms for GB-sized slabs) per call. Blocks are reused when the cached block
+// is at least the request and at most twice its size.
+// ---------------------------------------------------------------------------
+
+class DevicePool {
+  public:
+    static DevicePool& get() {
+        static DevicePool p;
+        return p;
+    }
+
+    // A cached block for the request, or nullptr (never allocates).
+    void* take_cached(int device, size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        std::lock_guard<std::mutex> lk(mu_);
+        auto& fl = free_[device];
+        auto it = fl.lower_bound(bytes);
+        if (it != fl.end() && it->first <= 2 * bytes) {
+            void* p = it->second;
+            sizes_[p] = it->first;
+            fl.erase(it);
+            return p;
+        }
+        return nullptr;
+    }
+
+    void* alloc(int device, size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        if (void* c = take_cached(device, bytes))
+            return c;
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            trim(device);
+            e = cudaMalloc(&p, bytes);
+        }
+        check_cuda(e, "cudaMalloc");
+        std::lock_guard<std::mutex> lk(mu_);
+        sizes_[p] = bytes;
+        return p;
+    }
+
+    void release(int device, void* p) {
+        if (!p)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = sizes_.find(p);
+        if (it == sizes_.end())
+            return;
+        free_[device].emplace(it->second, p);
+        sizes_.erase(it);
+    }
+
+    void trim(int device) {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& kv : free_[device])
+            cudaFree(kv.second);
+        free_[device].clear();
+    }
+    void trim_all() {
+        std::vector<int> devs;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto& kv : free_)
+                devs.push_back(kv.first);
+        }
+        for (int d : devs) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            trim(d);
+            cudaSetDevice(cur);
+        }
+    }
+
+  private:
+    std::mutex mu_;
+    std::map<int, std::multimap<size_t, void*>> free_;
+    std::map<void*, size_t> sizes_;
+};
+
+// Pinned host staging cache: cudaHostAlloc pins pages at ~4 GB/s (measured:
+// 2 GiB in 565 ms), which for two 153 MB staging slots would cost ~80 ms per
+// cbb_reconstruct call; blocks are kept for the next call (at most 6, reused
+// when at least the request and at most twice its size).
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool* p = new HostPool; // never destroyed: no CUDA calls at exit
+        return *p;
+    }
+    float* alloc(size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = free_.lower_bound(bytes);
+            if (it != free_.end() && it->first <= 2 * bytes) {
+                void* p = it->second;
+                sizes_[p] = it->first;
+                free_.erase(it);
+                return static_cast<float*>(p);
+            }
+        }
+        void* p = nullptr;
+        CK(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+        std::lock_guard<std::mutex> lk(mu_);
+        sizes_[p] = bytes;
+        return static_cast<float*>(p);
+    }
+    void release(void* p) {
+        if (!p)
+            return;
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = sizes_.find(p);
+        if (it == sizes_.end())
+            return;
+        free_.emplace(it->second, p);
+        sizes_.erase(it);
+        while (free_.size() > 6) { // drop the smallest
+            cudaFreeHost(free_.begin()->second);
+            free_.erase(free_.begin());
+        }
+    }
+    void trim() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& kv : free_)
+            cudaFreeHost(kv.second);
+        free_.clear();
+    }
+
+  private:
+    std::mutex mu_;
+    std::multimap<size_t, void*> free_;
+    std::map<void*, size_t> sizes_;
+};
+
+// Host copy into pinned staging, split over a few threads for large blocks
+// (a single thread moves ~5-10 GB/s, below the PCIe H2D rate).
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kChunk = size_t(8) << 20;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 8), (bytes + kChunk - 1) / kChunk);
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (bytes + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t off = t * per;
+        if (off >= bytes)
+            break;
+        const size_t len = std::min(per, bytes - off);
+        pool.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len);
+        });
+    }
+    for (auto& th : pool)
+        th.join();
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// Host <-> device copies of large blocks for pageable host memory: a plain
+// cudaMemcpyAsync from/to pageable memory is synchronous and staged by the
+// driver at a fraction of the link rate. Here 64 MB chunks go through two
+// pinned buffers, the host copies (parallel_memcpy) overlapping the DMA of
+// the neighbouring chunk. Pinned memory is copied directly (asynchronously).
+// ev: two events of the stream's device.
+struct ChunkedXfer {
+    static constexpr size_t kChunk = size_t(64) << 20;
+    float* buf[2] = {nullptr, nullptr};
+    ~ChunkedXfer() {
+        for (auto b : buf)
+            HostPool::get().release(b);
+    }
+    void ensure() {
+        for (auto& b : buf)
+            if (!b)
+                b = HostPool::get().alloc(kChunk);
+    }
+    // returns after the last chunk left the pageable source
+    void upload(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
+        if (bytes == 0)
+            return;
+        if (is_pinned(src)) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+            return;
+        }
+        ensure();
+        int k = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
+            const size_t len = std::min(kChunk, bytes - off);
+            CK(cudaEventSynchronize(ev[k])); // buf[k]'s previous DMA finished
+            parallel_memcpy(buf[k], static_cast<const char*>(src) + off, len);
+            CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf[k], len,
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(ev[k], st));
+        }
+    }
+    // pageable dst: blocks until all bytes arrived; pinned dst: asynchronous
+    void download(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
+        if (bytes == 0)
+            return;
+        if (is_pinned(dst)) {
+            CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+            return;
+        }
+        ensure();
+        const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+        auto issue = [&](size_t c) {
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            CK(cudaMemcpyAsync(buf[c & 1], static_cast<const char*>(src) + off, len,
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(ev[c & 1], st));
+        };
+        issue(0);
+        for (size_t c = 0; c < nchunks; ++c) {
+            if (c + 1 < nchunks)
+                issue(c + 1);
+            CK(cudaEventSynchronize(ev[c & 1]));
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            parallel_memcpy(static_cast<char*>(dst) + off, buf[c & 1], len);
+        }
+    }
+};
+
+} // namespace cbb

@@ -1,0 +1,807 @@
+// pipeline.cuh -- the staging pipeline: per-device workers (slab,
+// ring slots, streams), rotating upload roots and row-band peer copies,
+// resident tail pass, downloads, run statistics.
+// Internal part of libconebeam_b200.so: included, in this order, by
+// cbb_runtime.cu (one translation unit: runtime_common.cuh, launch.cuh,
+// memory.cuh, pipeline.cuh).
+#pragma once
+
+namespace cbb {
+
+// ---------------------------------------------------------------------------
+// Per-device worker: slab volume, raw/packed double buffers, streams, events.
+// ---------------------------------------------------------------------------
+
+struct Worker {
+    int device = 0;
+    int z_begin = 0, z_end = 0;
+    float* d_vol = nullptr;
+    float* d_raw[2] = {nullptr, nullptr};
+    void* d_packed[2] = {nullptr, nullptr};
+    int* d_err = nullptr;
+    cudaStream_t copy = nullptr, compute = nullptr;
+    cudaEvent_t h2d_done[2] = {}, raw_free[2] = {};
+    cudaEvent_t k_beg = nullptr, k_end = nullptr, c_beg = nullptr, c_end = nullptr;
+    double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
+    uint64_t guarded = 0;
+    bool started = false;
+    bool k_end_set = false; // k_end already recorded (resident tail)
+    // resident mode: every packed projection stays on the device; the head
+    // planes [z_begin, tail_lo) + [tail_hi, z_end) are updated while the
+    // batches stream in, the tail [tail_lo, tail_hi) afterwards while the
+    // head is copied back
+    void* d_packed_all = nullptr;
+    int tail_lo = 0, tail_hi = 0;
+    cudaEvent_t head_done = nullptr, tail_done = nullptr;
+    // detector rows this worker holds / packs (RowBand::full unless set_bands)
+    RowBand band;
+    size_t pk_bytes = 0;               // packed bytes per projection (band rows)
+    cudaEvent_t src_ready[2] = {};     // as root: raw slot filtered, peers may copy
+    cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
+    unsigned long long* d_counters = nullptr; // kCounterSlots culled-update counters
+    bool count_culled = false;
+
+    ~Worker() {
+        if (!copy)
+            return;
+        cudaSetDevice(device);
+        cudaStreamSynchronize(copy);
+        cudaStreamSynchronize(compute);
+        auto& pool = DevicePool::get();
+        pool.release(device, d_vol);
+        for (int i = 0; i < 2; ++i) {
+            pool.release(device, d_raw[i]);
+            pool.release(device, d_packed[i]);
+            cudaEventDestroy(h2d_done[i]);
+            cudaEventDestroy(raw_free[i]);
+            cudaEventDestroy(src_ready[i]);
+            cudaEventDestroy(xfer_ev[i]);
+        }
+        pool.release(device, d_err);
+        pool.release(device, d_counters);
+        pool.release(device, d_packed_all);
+        if (head_done)
+            cudaEventDestroy(head_done);
+        if (tail_done)
+            cudaEventDestroy(tail_done);
+        cudaEventDestroy(k_beg);
+        cudaEventDestroy(k_end);
+        cudaEventDestroy(c_beg);
+        cudaEventDestroy(c_end);
+        cudaStreamDestroy(copy);
+        cudaStreamDestroy(compute);
+    }
+};
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+}
+
+struct Pipeline {
+    cbb_volume_geometry g{};
+    int W = 0, H = 0;
+    cbb_options opt{};
+    std::vector<std::unique_ptr<Worker>> workers;
+    float* h_stage[2] = {nullptr, nullptr}; // pinned staging (batch x H x W)
+    ChunkedXfer xfer;                       // volume up/download for pageable buffers
+    int stage_fill = 0;                     // projections staged in the current slot
+    int slot = 0;                           // current staging / ring slot
+    std::vector<double> stage_mats;         // matrices of the staged batch
+    uint64_t submitted = 0;
+    uint64_t nbatch = 0;   // batches issued (root = nbatch mod workers)
+    size_t raw_bytes_per_proj = 0;
+    size_t packed_bytes_per_proj = 0;
+    bool resident = false;         // see Worker::d_packed_all
+    int resident_count = 0;
+    std::vector<double> all_mats;  // resident mode: every matrix, for the tail pass
+    const double* est_mats = nullptr; // matrices for choose_tails (else the first batch)
+    int est_n = 0;
+
+    // Resident mode for a stack of known size: when every packed projection
+    // fits in device memory (with 2 GB to spare), keep them all so a dense
+    // tail of each slab (choose_tails) can be back-projected after the stream
+    // ends while the rest is already copied to the host (hides most of the
+    // D2H).
+    void enable_resident(int count) {
+        if (std::getenv("CBB_NO_RESIDENT"))
+            return;
+        for (auto& w : workers)
+            if (w->z_end - w->z_begin < 16)
+                return;
+        std::vector<void*> blocks;
+        for (auto& w : workers) {
+            const size_t need = w->pk_bytes * (size_t)count;
+            CK(cudaSetDevice(w->device));
+            void* p = DevicePool::get().take_cached(w->device, need);
+            if (!p) {
+                size_t free_b = 0, total_b = 0;
+                CK(cudaMemGetInfo(&free_b, &total_b));
+                if (free_b >= need + (size_t(2) << 30))
+                    p = DevicePool::get().alloc(w->device, need);
+                else if (std::getenv("CBB_TRACE"))
+                    std::fprintf(stderr, "cbb: resident off, need %zu free %zu\n", need, free_b);
+            }
+            if (!p) {
+                for (size_t i = 0; i < blocks.size(); ++i)
+                    DevicePool::get().release(workers[i]->device, blocks[i]);
+                return;
+            }
+            blocks.push_back(p);
+        }
+        for (size_t i = 0; i < workers.size(); ++i) {
+            auto& w = workers[i];
+            CK(cudaSetDevice(w->device));
+            w->d_packed_all = blocks[i];
+            if (!w->head_done) {
+                CK(cudaEventCreate(&w->head_done));
+                CK(cudaEventCreateWithFlags(&w->tail_done, cudaEventDisableTiming));
+            }
+        }
+        resident = true;
+        resident_count = count;
+        all_mats.assign(12 * (size_t)count, 0.0);
+    }
+
+    // Picks each worker's tail: the contiguous run of 8-plane groups with the
+    // fewest planes that holds ~kTailFrac of the slab's estimated work. Work
+    // per group = fraction of sampled (x, y, projection) positions that land
+    // on the detector (the rest is culled warp by warp) + a fixed overhead,
+    // sampled on a 16 x 16 grid at the group's centre plane for up to 8 of
+    // the given projections. A dense tail keeps its D2H short while its
+    // compute hides the head's D2H.
+    void choose_tails(const double* mats, int n) {
+        double frac = 0.12;
+        if (const char* e = std::getenv("CBB_TAIL_FRAC"))
+            frac = std::atof(e);
+        const int L = g.edge_voxels, S = 16, NP = std::min(n, 8);
+        for (auto& w : workers) {
+            std::vector<double> gw;
+            std::vector<int> gz;
+            for (int z = w->z_begin; z < w->z_end; z += 8) {
+                const int pz = std::min(8, w->z_end - z);
+                const double zc = g.origin_mm + (z + (pz - 1) * 0.5) * g.voxel_mm;
+                int on = 0;
+                for (int k = 0; k < NP; ++k) {
+                    const double* a = mats + 12 * (size_t)((long long)k * n / NP);
+                    for (int j = 0; j < S; ++j)
+                        for (int i = 0; i < S; ++i) {
+                            const double x = g.origin_mm + (L - 1) * (i / (S - 1.0)) * g.voxel_mm;
+                            const double y = g.origin_mm + (L - 1) * (j / (S - 1.0)) * g.voxel_mm;
+                            const double u = a[0] * x + a[3] * y + a[6] * zc + a[9];
+                            const double v = a[1] * x + a[4] * y + a[7] * zc + a[10];
+                            const double ww = a[2] * x + a[5] * y + a[8] * zc + a[11];
+                            const double ix = u / ww, iy = v / ww;
+                            on += ix > -2 && ix < W && iy > -2 && iy < H;
+                        }
+                }
+                gw.push_back(pz * ((double)on / (NP * S * S) + 0.05));
+                gz.push_back(z);
+            }
+            gz.push_back(w->z_end);
+            const int G = (int)gw.size();
+            double total = 0.0;
+            for (double x : gw)
+                total += x;
+            int best_i = G - 1, best_j = G, best_planes = 1 << 30;
+            for (int i = 0; i < G; ++i) {
+                double s = 0.0;
+                for (int j = i; j < G; ++j) {
+                    s += gw[j];
+                    if (s >= frac * total) {
+                        const int planes = gz[j + 1] - gz[i];
+                        if (planes < best_planes && !(i == 0 && j == G - 1)) {
+                            best_planes = planes;
+                            best_i = i;
+                            best_j = j + 1;
+                        }
+                        break;
+                    }
+                }
+            }
+            w->tail_lo = gz[best_i];
+            w->tail_hi = gz[best_j];
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: device %d slab [%d, %d) tail [%d, %d)\n", w->device,
+                             w->z_begin, w->z_end, w->tail_lo, w->tail_hi);
+        }
+    }
+
+    ~Pipeline() {
+        workers.clear();
+        for (int i = 0; i < 2; ++i)
+            HostPool::get().release(h_stage[i]);
+    }
+
+    void init(const cbb_volume_geometry& geom, int width, int height, const cbb_options& o,
+              const float* initial_volume) {
+        g = geom;
+        W = width;
+        H = height;
+        opt = o;
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (ndev < 1)
+            fail(CBB_ERR_INTERNAL, "no CUDA device available");
+        if (opt.slab_end > g.edge_voxels)
+            fail(CBB_ERR_INVALID, "options: slab_end %d beyond L = %d", opt.slab_end,
+                 g.edge_voxels);
+        const int s0 = opt.slab_end ? opt.slab_begin : 0;
+        const int s1 = opt.slab_end ? opt.slab_end : g.edge_voxels;
+        int ng = opt.num_gpus > 0 ? opt.num_gpus : ndev;
+        ng = std::min(ng, s1 - s0);
+        if (!opt.device_ids && ng > ndev)
+            fail(CBB_ERR_INVALID, "options: num_gpus %d exceeds %d visible devices", ng, ndev);
+        raw_bytes_per_proj = (size_t)W * H * sizeof(float);
+        packed_bytes_per_proj = (size_t)quad_pitch_cells(W) * quad_rows(H) * 16;
+        const int L = g.edge_voxels;
+        const size_t plane = (size_t)L * L;
+        for (int i = 0; i < ng; ++i) {
+            auto w = std::make_unique<Worker>();
+            w->device = opt.device_ids ? opt.device_ids[i] : i;
+            if (w->device < 0 || w->device >= ndev)
+                fail(CBB_ERR_INVALID, "options: device id %d not visible", w->device);
+            w->z_begin = s0 + (int)((long long)(s1 - s0) * i / ng);
+            w->z_end = s0 + (int)((long long)(s1 - s0) * (i + 1) / ng);
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));
+            for (int s = 0; s < 2; ++s) {
+                CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->src_ready[s], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->xfer_ev[s], cudaEventDisableTiming));
+                w->d_raw[s] = static_cast<float*>(
+                    DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
+                w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
+            }
+            w->band = RowBand::full(H);
+            w->pk_bytes = packed_bytes_per_proj;
+            CK(cudaEventCreate(&w->k_beg));
+            CK(cudaEventCreate(&w->k_end));
+            CK(cudaEventCreate(&w->c_beg));
+            CK(cudaEventCreate(&w->c_end));
+            const size_t slab = plane * (w->z_end - w->z_begin);
+            w->d_vol = static_cast<float*>(
+                DevicePool::get().alloc(w->device, std::max<size_t>(slab, 1) * sizeof(float)));
+            w->d_err = static_cast<int*>(DevicePool::get().alloc(w->device, sizeof(int)));
+            CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
+            const size_t cbytes = sizeof(unsigned long long) * kCounterSlots;
+            w->d_counters = static_cast<unsigned long long*>(
+                DevicePool::get().alloc(w->device, cbytes));
+            CK(cudaMemsetAsync(w->d_counters, 0, cbytes, w->compute));
+            w->count_culled = opt.count_culled != 0;
+            CK(cudaEventRecord(w->c_beg, w->copy));
+            if (initial_volume && !opt.volume_is_zero)
+                xfer.upload(w->d_vol, initial_volume + plane * w->z_begin, slab * sizeof(float),
+                            w->copy, w->xfer_ev);
+            else
+                CK(cudaMemsetAsync(w->d_vol, 0, slab * sizeof(float), w->copy));
+            CK(cudaEventRecord(w->c_end, w->copy));
+            CK(cudaStreamWaitEvent(w->compute, w->c_end, 0));
+            workers.push_back(std::move(w));
+        }
+        stage_mats.assign(12 * (size_t)opt.batch, 0.0);
+        // band copies go straight over NVLink where the devices allow it
+        for (auto& a : workers)
+            for (auto& b : workers) {
+                int can = 0;
+                if (a->device == b->device ||
+                    cudaDeviceCanAccessPeer(&can, b->device, a->device) != cudaSuccess || !can)
+                    continue;
+                CK(cudaSetDevice(b->device));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(a->device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled)
+                    cudaGetLastError();
+                else
+                    CK(e);
+            }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->h2d_s += elapsed_s(w->c_beg, w->c_end);
+        }
+    }
+
+    // Issues one batch of n projections from host memory src (pinned or not)
+    // to every worker. The caller guarantees src stays valid until the
+    // corresponding h2d_done events complete (wait_slot).
+    void issue(const float* src, const double* mats, int n) {
+        const size_t bytes = raw_bytes_per_proj * n;
+        if (resident && submitted == 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: choose_tails %.2f ms\n",
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
+        }
+        // Batch k is uploaded once, by the root worker k mod G, and each
+        // other worker copies its row band from the root's raw slot (peer
+        // copy over NVLink; a plain device copy when both are one device).
+        const int G = (int)workers.size();
+        Worker& root = *workers[nbatch % G];
+        // raw[slot] of worker w may still be read by its own pack of batch
+        // k-2 and, if w was that batch's root, by the other workers' band copies
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
+            for (auto& o : workers)
+                if (o != w)
+                    CK(cudaStreamWaitEvent(w->copy, o->h2d_done[slot], 0));
+        }
+        CK(cudaSetDevice(root.device));
+        CK(cudaMemcpyAsync(root.d_raw[slot], src, bytes, cudaMemcpyHostToDevice, root.copy));
+        CK(cudaEventRecord(root.h2d_done[slot], root.copy));
+        CK(cudaStreamWaitEvent(root.compute, root.h2d_done[slot], 0));
+        start_timing(root);
+        // the root sees the whole batch: it checks the pixels its band skips
+        if (!root.band.is_full(H))
+            launch_check_finite(root.d_raw[slot], (long long)n * W * H, root.d_err, root.compute);
+        cudaEvent_t ready = root.h2d_done[slot];
+        if (opt.ramp_filter) {
+            ramp_filter_device(root.d_raw[slot], root.d_raw[slot], W, H, n, opt.filter_pixel_mm,
+                               root.compute);
+            CK(cudaEventRecord(root.src_ready[slot], root.compute));
+            ready = root.src_ready[slot];
+        }
+        for (auto& w : workers) {
+            if (w.get() == &root)
+                continue;
+            CK(cudaSetDevice(w->device));
+            CK(cudaStreamWaitEvent(w->copy, ready, 0));
+            copy_band(root, *w, slot, n);
+            CK(cudaEventRecord(w->h2d_done[slot], w->copy));
+            CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
+            start_timing(*w);
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            void* packed = resident ? static_cast<char*>(w->d_packed_all) + w->pk_bytes * submitted
+                                    : w->d_packed[slot];
+            if (w.get() == &root)
+                launch_pack_band(w->d_raw[slot], 0, H, (long long)W * H, W, H, n, packed, w->band,
+                                 w->compute, w->d_err);
+            else
+                launch_pack_band(w->d_raw[slot], w->band.r0, w->band.rn,
+                                 (long long)w->band.rn * W, W, H, n, packed, w->band, w->compute,
+                                 w->d_err);
+            CK(cudaEventRecord(w->raw_free[slot], w->compute));
+            // resident: the head, i.e. the slab minus the tail planes
+            w->guarded += launch_backproject(w->d_vol, g, w->z_begin, w->z_end, packed, W, H, n,
+                                             mats, opt, w->d_err, w->compute,
+                                             resident ? w->tail_lo : 0, resident ? w->tail_hi : 0,
+                                             &w->band, w->count_culled ? w->d_counters : nullptr);
+        }
+        ++nbatch;
+        if (resident)
+            std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
+        submitted += n;
+        slot ^= 1;
+    }
+
+    void start_timing(Worker& w) {
+        if (!w.started) {
+            CK(cudaEventRecord(w.k_beg, w.compute));
+            w.started = true;
+        }
+    }
+
+    // Rows [band.r0, band.r0 + band.rn) of the batch's n projections, from the
+    // root's full raw slot to w's band slot (projection stride rn * W), one
+    // strided peer copy on w's copy stream.
+    void copy_band(const Worker& root, Worker& w, int s, int n) {
+        const RowBand& b = w.band;
+        if (b.rn <= 0)
+            return;
+        cudaMemcpy3DPeerParms p = {};
+        const size_t row_bytes = (size_t)b.rn * W * sizeof(float);
+        p.srcPtr = make_cudaPitchedPtr(root.d_raw[s] + (size_t)b.r0 * W, raw_bytes_per_proj,
+                                       row_bytes, n);
+        p.srcDevice = root.device;
+        p.dstPtr = make_cudaPitchedPtr(w.d_raw[s], row_bytes, row_bytes, n);
+        p.dstDevice = w.device;
+        p.extent = make_cudaExtent(row_bytes, n, 1);
+        CK(cudaMemcpy3DPeerAsync(&p, w.copy));
+    }
+
+    RowBand band_for(const Worker& w, const double* mats, int count) const {
+        if (std::getenv("CBB_NO_BANDS"))
+            return RowBand::full(H);
+        return row_band_for(g, W, H, w.z_begin, w.z_end, mats, count);
+    }
+
+    // Sets every worker's row band for a stack whose matrices are all known.
+    void set_bands(const double* mats, int count) {
+        for (auto& w : workers) {
+            w->band = band_for(*w, mats, count);
+            w->pk_bytes = (size_t)quad_pitch_cells(W) * w->band.qn * 16;
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: device %d slab [%d, %d) rows [%d, %d) cells %d of %d\n",
+                             w->device, w->z_begin, w->z_end, w->band.r0,
+                             w->band.r0 + w->band.rn, w->band.qn, quad_rows(H));
+        }
+    }
+
+    // Host-side proof that every batch of the tail pass runs unguarded (no
+    // possible w == 0 error), so the head may be copied out before the tail
+    // is computed.
+    bool tail_is_safe(const Worker& w) const {
+        const float Of = (float)g.origin_mm, MMf = (float)g.voxel_mm;
+        const double cxy = min_nonzero_coord(Of, MMf, 0, g.edge_voxels);
+        const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, w.tail_lo, w.tail_hi)};
+        for (int p = 0; p < resident_count; ++p)
+            if (!projection_is_safe(all_mats.data() + 12 * (size_t)p, g, w.tail_lo, w.tail_hi,
+                                    cmin))
+                return false;
+        return true;
+    }
+
+    // Blocks until no device still reads the staging slot s.
+    void wait_slot(int s) {
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->h2d_done[s]));
+        }
+    }
+
+    // Pinned staging for pageable sources, allocated on first use only.
+    void ensure_staging() {
+        for (int s = 0; s < 2; ++s)
+            if (!h_stage[s])
+                h_stage[s] = HostPool::get().alloc(raw_bytes_per_proj * opt.batch);
+    }
+
+    void stage_one(const float* img, const double* m) {
+        ensure_staging();
+        if (stage_fill == 0)
+            wait_slot(slot);
+        std::memcpy(h_stage[slot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
+        std::memcpy(stage_mats.data() + 12 * (size_t)stage_fill, m, 12 * sizeof(double));
+        if (++stage_fill == opt.batch)
+            flush();
+    }
+
+    void flush() {
+        if (stage_fill == 0)
+            return;
+        issue(h_stage[slot], stage_mats.data(), stage_fill);
+        stage_fill = 0;
+    }
+
+    // Size of the batch starting at projection `first` of a stream: 4, 4, 8,
+    // 16, ... up to opt.batch, so the first back-projection starts after a
+    // small upload instead of a full batch (pipeline fill). Batch boundaries
+    // do not change any result: each voxel still accumulates the projections
+    // one by one in stack order.
+    int batch_at(int first, int count) const {
+        return std::min({opt.batch, std::max(4, first), count - first});
+    }
+
+    // Whole-stack submission straight from the caller's buffer: pinned
+    // buffers are copied asynchronously in place, pageable ones are staged
+    // through the pinned double buffer.
+    // First submission of a stack whose matrices are all known: row bands,
+    // resident mode, tail estimate.
+    void begin_stack(const double* mats, int count) {
+        if (submitted != 0)
+            return;
+        const auto t0 = std::chrono::steady_clock::now();
+        set_bands(mats, count);
+        enable_resident(count);
+        if (std::getenv("CBB_TRACE"))
+            std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - t0).count());
+        est_mats = mats;
+        est_n = count;
+    }
+
+    void submit_stack(const float* imgs, const double* mats, int count) {
+        begin_stack(mats, count);
+        cudaPointerAttributes attr;
+        bool pinned = false;
+        if (cudaPointerGetAttributes(&attr, imgs) == cudaSuccess)
+            pinned = attr.type == cudaMemoryTypeHost;
+        else
+            cudaGetLastError();
+        for (int first = 0, n = 0; first < count; first += n) {
+            n = batch_at(first, count);
+            const float* src = imgs + (size_t)first * W * H;
+            if (pinned) {
+                issue(src, mats + 12 * (size_t)first, n);
+            } else {
+                ensure_staging();
+                wait_slot(slot);
+                parallel_memcpy(h_stage[slot], src, raw_bytes_per_proj * n);
+                issue(h_stage[slot], mats + 12 * (size_t)first, n);
+            }
+        }
+    }
+
+    // Projections in separate host buffers (the reference's ProjectionStack):
+    // each batch is gathered into a pinned staging slot by a few threads
+    // (whole projections per thread) while the devices process the previous
+    // batch.
+    void submit_images(const float* const* imgs, const double* mats, int count) {
+        begin_stack(mats, count);
+        ensure_staging();
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (int first = 0, n = 0; first < count; first += n) {
+            n = batch_at(first, count);
+            wait_slot(slot);
+            float* dst = h_stage[slot];
+            const int nt = (int)std::min<unsigned>(std::min(8u, hw), (unsigned)n);
+            std::vector<std::thread> pool;
+            for (int t = 0; t < nt; ++t)
+                pool.emplace_back([&, t] {
+                    for (int j = t; j < n; j += nt)
+                        std::memcpy(dst + (size_t)j * W * H, imgs[first + j], raw_bytes_per_proj);
+                });
+            for (auto& th : pool)
+                th.join();
+            issue(dst, mats + 12 * (size_t)first, n);
+        }
+    }
+
+    // Streams the projection records of an open CBPS file (proj/src/dataset.cpp:
+    // 155-212 layout: per record 12 little-endian f64 then W*H f32) straight
+    // into the pinned staging slots: record i's image goes to its place in
+    // the batch, its matrix to a small host array. Reads of batch k+1 run on
+    // the host while the devices process batch k; each batch is read by a
+    // few threads with pread.
+    void submit_file(int fd, int count, uint64_t header_bytes, uint64_t rec_bytes) {
+        if (submitted == 0)
+            enable_resident(count);
+        ensure_staging();
+        std::vector<double> mats(12 * (size_t)opt.batch);
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int nt = (int)std::min<unsigned>(8, hw);
+        // the records are copied out of a read-only mapping of the file
+        // (page-cache pages mapped, no per-call kernel copy); pread when the
+        // file cannot be mapped
+        const uint64_t file_bytes = header_bytes + rec_bytes * (uint64_t)count;
+        const char* map = nullptr;
+        if (!std::getenv("CBB_FILE_PREAD")) {
+            void* m = ::mmap(nullptr, file_bytes, PROT_READ, MAP_SHARED, fd, 0);
+            if (m != MAP_FAILED) {
+                map = static_cast<const char*>(m);
+                ::madvise(m, file_bytes, MADV_SEQUENTIAL);
+            }
+        }
+        struct Unmap {
+            const char* p;
+            uint64_t n;
+            ~Unmap() {
+                if (p)
+                    ::munmap(const_cast<char*>(p), n);
+            }
+        } unmap{map, file_bytes};
+        double t_wait = 0, t_read = 0, t_issue = 0;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms_since = [](std::chrono::steady_clock::time_point t) {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t)
+                .count();
+        };
+        for (int first = 0, n = 0; first < count; first += n) {
+            n = batch_at(first, count);
+            auto t0 = now();
+            wait_slot(slot);
+            t_wait += ms_since(t0);
+            t0 = now();
+            float* dst = h_stage[slot];
+            std::vector<std::thread> pool;
+            std::vector<int> bad(nt, 0);
+            for (int t = 0; t < nt; ++t)
+                pool.emplace_back([&, t] {
+                    for (int j = t; j < n; j += nt) {
+                        const uint64_t off = header_bytes + rec_bytes * (uint64_t)(first + j);
+                        if (map) {
+                            std::memcpy(mats.data() + 12 * (size_t)j, map + off, 96);
+                            std::memcpy(dst + (size_t)j * W * H, map + off + 96, rec_bytes - 96);
+                        } else if (!pread_all(fd, mats.data() + 12 * (size_t)j, 96, off) ||
+                                   !pread_all(fd, dst + (size_t)j * W * H, rec_bytes - 96,
+                                              off + 96)) {
+                            bad[t] = 1;
+                        }
+                    }
+                });
+            for (auto& th : pool)
+                th.join();
+            for (int b : bad)
+                if (b)
+                    fail(CBB_ERR_TRUNCATED, "file ends inside projection intensities");
+            validate_matrices(mats.data(), n);
+            t_read += ms_since(t0);
+            t0 = now();
+            issue(dst, mats.data(), n);
+            t_issue += ms_since(t0);
+        }
+        if (std::getenv("CBB_TRACE"))
+            std::fprintf(stderr, "cbb: file stream: wait %.1f ms, read %.1f ms, issue %.1f ms\n",
+                         t_wait, t_read, t_issue);
+    }
+
+    static bool pread_all(int fd, void* buf, uint64_t bytes, uint64_t off) {
+        char* p = static_cast<char*>(buf);
+        while (bytes) {
+            const ssize_t r = ::pread(fd, p, bytes, (off_t)off);
+            if (r <= 0)
+                return false;
+            p += r;
+            off += (uint64_t)r;
+            bytes -= (uint64_t)r;
+        }
+        return true;
+    }
+
+    // Waits for all work, checks the w == 0 flag, downloads slabs into vol_out.
+    // Synchronizes every worker's compute stream and raises the first error
+    // the kernels flagged (nothing has been written to the host yet).
+    void check_errors(bool close_timing) {
+        int err_any = 0;
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (close_timing && w->started && !w->k_end_set)
+                CK(cudaEventRecord(w->k_end, w->compute));
+            w->k_end_set = false;
+            CK(cudaStreamSynchronize(w->compute));
+            if (close_timing && w->started) {
+                w->kernel_s += elapsed_s(w->k_beg, w->k_end);
+                w->started = false;
+            }
+            int e = 0;
+            CK(cudaMemcpy(&e, w->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+            err_any |= e;
+        }
+        if (err_any & 2) // ProjectionImage::validate (proj/src/dataset.cpp:123-129)
+            fail(CBB_ERR_INVALID, "ProjectionImage contains non-finite values");
+        if (err_any & 1)
+            fail(CBB_ERR_GEOMETRY, "backprojection hit a voxel with w == 0");
+    }
+
+    // Waits for all work, checks the error flags, downloads slabs into vol_out.
+    void finish(float* vol_out) {
+        flush();
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        if (resident) {
+            finish_resident(vol_out);
+            return;
+        }
+        check_errors(true);
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            const size_t slab = plane * (w->z_end - w->z_begin);
+            CK(cudaEventRecord(w->c_beg, w->copy));
+            xfer.download(vol_out + plane * w->z_begin, w->d_vol, slab * sizeof(float), w->copy,
+                          w->xfer_ev);
+            CK(cudaEventRecord(w->c_end, w->copy));
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->d2h_s += elapsed_s(w->c_beg, w->c_end);
+        }
+    }
+
+    // Resident mode: the head planes are complete once the stream has been
+    // consumed; the tail planes are back-projected from the resident packed
+    // projections while the head is copied to the host (copy stream). The
+    // head is released early only when no tail batch can raise an error
+    // (tail_is_safe, no guarded head batch); otherwise everything is checked
+    // before any byte reaches vol_out.
+    void finish_resident(float* vol_out) {
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        check_errors(false);
+        bool overlap = true;
+        for (auto& w : workers)
+            overlap = overlap && w->guarded == 0 && tail_is_safe(*w);
+        const bool trace = std::getenv("CBB_TRACE") != nullptr;
+        cudaEvent_t t_tail = nullptr;
+        auto d2h = [&](Worker& w, int z0, int z1) {
+            if (z1 > z0)
+                xfer.download(vol_out + plane * z0, w.d_vol + plane * (z0 - w.z_begin),
+                              plane * (z1 - z0) * sizeof(float), w.copy, w.xfer_ev);
+        };
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (trace && w == workers.front()) {
+                CK(cudaEventCreate(&t_tail));
+                CK(cudaEventRecord(t_tail, w->compute));
+            }
+            w->guarded += launch_backproject(
+                w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
+                w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
+                w->compute, 0, 0, &w->band, w->count_culled ? w->d_counters : nullptr);
+            CK(cudaEventRecord(w->tail_done, w->compute));
+            if (w->started) { // kernel time ends with the tail, not the downloads
+                CK(cudaEventRecord(w->k_end, w->compute));
+                w->k_end_set = true;
+            }
+        }
+        if (overlap) {
+            // the tail runs on the compute streams (launched above) while the
+            // head is copied out; then the tail (no error can arise in it:
+            // tail_is_safe). Downloads into pageable memory block this
+            // thread chunk by chunk, the tail kernels keep running.
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
+                CK(cudaEventRecord(w->c_beg, w->copy));
+                d2h(*w, w->z_begin, w->tail_lo);
+                d2h(*w, w->tail_hi, w->z_end);
+                CK(cudaEventRecord(w->head_done, w->copy));
+            }
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
+                CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
+                d2h(*w, w->tail_lo, w->tail_hi);
+                CK(cudaEventRecord(w->c_end, w->copy));
+            }
+        }
+        // closes the kernel timing; with overlap this only re-checks flags
+        // that cannot be set (pack errors were checked above)
+        check_errors(true);
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            if (!overlap) {
+                CK(cudaEventRecord(w->c_beg, w->copy));
+                d2h(*w, w->z_begin, w->z_end);
+                CK(cudaEventRecord(w->c_end, w->copy));
+            }
+        }
+        for (auto& w : workers) {
+            CK(cudaSetDevice(w->device));
+            CK(cudaEventSynchronize(w->c_end));
+            w->d2h_s += elapsed_s(w->c_beg, w->c_end);
+        }
+        if (t_tail) {
+            auto& w = *workers.front();
+            std::fprintf(stderr,
+                         "cbb: resident, overlap %d, tail [%d, %d): k_beg->tail %.2f ms, "
+                         "head d2h %.2f ms, k_beg->k_end %.2f ms, k_beg->c_end %.2f ms\n",
+                         (int)overlap, w.tail_lo, w.tail_hi, elapsed_s(w.k_beg, t_tail) * 1e3,
+                         overlap ? elapsed_s(w.c_beg, w.head_done) * 1e3 : 0.0,
+                         elapsed_s(w.k_beg, w.k_end) * 1e3, elapsed_s(w.k_beg, w.c_end) * 1e3);
+            cudaEventDestroy(t_tail);
+        }
+        resident = false;
+    }
+
+    void fill_stats(cbb_run_stats* st, double total) {
+        if (!st)
+            return;
+        std::memset(st, 0, sizeof *st);
+        uint64_t culled = 0;
+        for (auto& w : workers) {
+            std::vector<unsigned long long> c(kCounterSlots);
+            CK(cudaSetDevice(w->device));
+            CK(cudaMemcpy(c.data(), w->d_counters, sizeof(unsigned long long) * c.size(),
+                          cudaMemcpyDeviceToHost));
+            for (auto x : c)
+                culled += x;
+        }
+        st->culled_updates = culled;
+        st->total_seconds = total;
+        st->num_gpus = (int32_t)workers.size();
+        uint64_t planes = 0;
+        for (const auto& w : workers)
+            planes += (uint64_t)(w->z_end - w->z_begin);
+        st->voxel_updates = (uint64_t)g.edge_voxels * g.edge_voxels * planes * submitted;
+        for (size_t i = 0; i < workers.size(); ++i) {
+            const auto& w = *workers[i];
+            st->h2d_seconds = std::max(st->h2d_seconds, w.h2d_s);
+            st->kernel_seconds = std::max(st->kernel_seconds, w.kernel_s);
+            st->d2h_seconds = std::max(st->d2h_seconds, w.d2h_s);
+            st->guarded_batches += w.guarded;
+            if (i < 8)
+                st->per_gpu_kernel_seconds[i] = w.kernel_s;
+        }
+        st->culled_fraction = !opt.count_culled ? -1.0
+                              : st->voxel_updates
+                                  ? (double)st->culled_updates / (double)st->voxel_updates
+                                  : 0.0;
+    }
+};
+
+} // namespace cbb
