@@ -13,7 +13,7 @@ projections into the gather layout, back-project them in batches of 32.
   value : inputs resident in HBM; device-timed with CUDA events; max over ranks.
   e2e   : the public host API (cbb_reconstruct through reconstruct_arrays) from
           pinned host projections to the host volume, H2D + kernels + D2H.
-Inputs (2.4 GB raw + 9.6 GB packed) exceed the 126 MB L2, so no flush is needed.
+Inputs (2.4 GB raw + 11.3 GB packed) exceed the 126 MB L2, so no flush is needed.
 Multi-GPU (torchrun): each rank owns a z-slab of the same volume (strong
 scaling); no data-path collective in `value`.
 """
@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+from types import SimpleNamespace
 import os
 import statistics
 import subprocess
@@ -371,42 +372,12 @@ def run_ours(args):
     total_updates = L ** 3 * n  # all ranks together
     value = total_updates / (ms_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (bp_kernel), per launch
-    bp_launch_ms = statistics.mean(bp_ms) / nbatch
-    updates_per_launch = (z1 - z0) * L * L * args.batch
-    peaks, peak_src = measured_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lane-ops/s (Tops) at max clock
-    achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
-    sm_load = clocks.get("sm_mhz") or sm_max
-    hbm_bytes = 8 * (z1 - z0) * L * L + args.batch * nb  # volume rmw + packed inputs
-    traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        rec = json.load(open(tpath)).get(f"{cfg.name}/{args.mode}")
-        if rec and world == 1:
-            traffic = rec["dram_bytes_per_launch"]
-            traffic_src = f"profiles/{rec['source']} (ncu --set full, one launch)"
-    roofline = {
-        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 3),
-        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
-        "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(hbm_bytes),
-        "peak_basis": f"{nsm} SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, "
-                      f"{peak_src} peaks file); 34 algorithmic FP32 ops per voxel update",
-        "frac_at_load_clock": round(achieved / (nsm * 128 * sm_load * 1e6 / 1e12), 4),
-        "gups_per_launch": round(updates_per_launch / (bp_launch_ms * 1e-3) / 1e9, 2),
-        "launch_ms": round(bp_launch_ms, 4),
-        "alongside": {
-            "gather": {"achieved_GBps": round(updates_per_launch * GATHER_BYTES_PER_UPDATE /
-                                              (bp_launch_ms * 1e-3) / 1e9, 1),
-                       "peak_GBps": round(nsm * 128 * sm_max * 1e6 / 1e9, 1),
-                       "unit": "L1 B/s (128 B/clk/SM)"},
-            "hbm": {"algorithmic_GBps": round(hbm_bytes / (bp_launch_ms * 1e-3) / 1e9, 1),
-                    "peak_GBps": peaks.get("hbm_gbs")},
-        },
-    }
-
+    c = SimpleNamespace(pkg=pkg, torch=torch, dist=dist, dev=dev, rank=rank, world=world,
+                        local=local, args=args, cfg=cfg, mode=mode, g=g, mats=mats, imgs=imgs,
+                        L=L, n=n, H=H, W=W, slabs=slabs, z0=z0, z1=z1, band=band, nb=nb,
+                        packed=packed, vol=vol, err=err, stream=stream,
+                        total_updates=total_updates)
+    roofline = roofline_entry(c, bp_ms, nbatch, clocks)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GUp/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -429,179 +400,250 @@ def run_ours(args):
         "roofline": roofline,
     }
 
-    # secondary device-resident measurements (same projections, same packed
-    # buffer): the other arithmetic mode on this workload, and the 1024^3
-    # volume of config 3 (configs 0-3 share the scan)
     if not args.no_secondary:
-        def measure(geom, mode_id, steps, slab):
-            zz0, zz1 = slab
-            LL = geom.edge_voxels
-            v2 = torch.empty(((zz1 - zz0), LL, LL), dtype=torch.float32, device=dev)
-            o2 = pkg.Options(batch=args.batch, mode=mode_id)
-
-            b2 = pkg.row_band_for_slab(geom, W, H, zz0, zz1, mats)
-
-            def st2():
-                v2.zero_()
-                pkg.pack_device_band(imgs, b2, packed, err, stream)
-                pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream,
-                                       band=b2)
-            for _ in range(2):
-                st2()
-            if dist:
-                dist.barrier()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(steps):
-                st2()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ms = a.elapsed_time(b) / steps
-            if dist:
-                t = torch.tensor([ms], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = float(t.item())
-            res = {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
-                   "ms_per_step": round(ms, 3)}
-            if geom is g and mode_id != mode:
-                # full-size agreement of the two modes on the GPU (exact mode is
-                # bitwise the reference's result, see tests/test_gpu_parity.py)
-                dff = pkg.compare_volumes_device(v2, vol)
-                res["vs_exact" if mode_id == pkg.MODE_FAST else "vs_fast"] = {
-                    k: dff[k] for k in ("rel_l2", "max_abs_over_range", "bitwise_different")}
-            del v2
-            return res
-
-        other = "fast" if args.mode == "exact" else "exact"
-        sec = [dict(workload=cfg.name, mode=other,
-                    **measure(g, pkg.MODE_FAST if other == "fast" else pkg.MODE_EXACT,
-                              args.steps, (z0, z1)))]
-        if args.config != 3 and cfg.width == synth.CONFIGS[3].width:
-            g3 = synth.CONFIGS[3].geometry
-            if world > 1:
-                from paper_1401_3615_b200.distributed import balanced_slabs, plane_work
-                sl3 = balanced_slabs(plane_work(g3, mats, W, H), world)[rank]
-            else:
-                sl3 = (0, g3.edge_voxels)
-            sec.append(dict(workload=synth.CONFIGS[3].name, mode=args.mode,
-                            **measure(g3, mode, 3, sl3)))
-        # north_star's hardware-texture side number (not parity-exact)
-        from paper_1401_3615_b200.backproject import backproject_texture_device
-        vt = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
-
-        def st_tex():
-            vt.zero_()
-            backproject_texture_device(vt, g, z0, z1, imgs, mats, stream)
-        st_tex()
-        torch.cuda.synchronize()
-        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ta.record(stream)
-        for _ in range(3):
-            st_tex()
-        tb.record(stream)
-        torch.cuda.synchronize()
-        ms_t = ta.elapsed_time(tb) / 3
-        dtex = pkg.compare_volumes_device(vt, vol)  # vs this run's main-mode volume
-        sec.append({"workload": cfg.name, "mode": "texture (side number, not parity-exact)",
-                    "value": round(L ** 3 * n / (ms_t * 1e-3) / 1e9, 3), "unit": "GUp/s",
-                    "ms_per_step": round(ms_t, 3),
-                    "vs_" + args.mode: {k: dtex[k] for k in ("rel_l2", "max_abs_over_range")}})
-        del vt
-        line["secondary"] = sec
-        torch.cuda.empty_cache()
-        pkg.release_cached_memory()  # e.g. the texture variant's layered array
-
-    # e2e through the public host API: pinned host projections -> host volume
+        line["secondary"] = secondary_entries(c)
     if not args.no_e2e:
-        imgs_h = imgs.cpu().pin_memory()
+        c.packed = None
         del packed
-        torch.cuda.empty_cache()
-        imgs_np = imgs_h.numpy()
-        # the host volume (pinned): this rank's slab planes are written by the call
-        vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
-        buf = vol_h.numpy()
-        e2e_opt = pkg.Options(batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
-                              volume_is_zero=True, slab=(z0, z1))
-        if world == 1:
-            # the drop-in C ABI: cbb_reconstruct with host buffers
-            def e2e_call():
-                buf[z0:z1] = 0.0
-                t0 = time.perf_counter()
-                st = pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)
-                return time.perf_counter() - t0, st
-            h2d = imgs_h.numel() * 4 + mats.nbytes
-            path = "cbb_reconstruct (C ABI), pinned host buffers"
-        else:
-            # one process per GPU: batch b uploaded by rank b % N, NCCL broadcast
-            from paper_1401_3615_b200.distributed import DistributedReconstructor, batch_roots
-            rec = DistributedReconstructor(g, W, H, batch=args.batch, slabs=slabs,
-                                           options=e2e_opt)
-
-            def e2e_call():
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                slab = rec.reconstruct(imgs_h, mats)
-                return time.perf_counter() - t0, {"slab_planes": int(slab.shape[0])}
-            h2d = sum(n for _, n, r in batch_roots(n_proj, args.batch, world) if r == rank) \
-                * H * W * 4 + mats.nbytes
-            path = "DistributedReconstructor: 1/N of batches uploaded per rank + NCCL broadcast"
-        e2e_call()  # warm-up
-        if dist:
-            dist.barrier()
-        e2e_s = []
-        stats = None
-        for _ in range(max(1, min(args.steps, 3))):
-            dt, stats = e2e_call()
-            e2e_s.append(dt)
-        e2e_t = statistics.median(e2e_s)
-        if dist:
-            t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t.item())
-        line["e2e"] = {"value": round(total_updates / e2e_t / 1e9, 3), "unit": "GUp/s",
-                       "h2d_bytes_per_step": int(h2d),
-                       "d2h_bytes_per_step": int((z1 - z0) * L * L * 4),
-                       "seconds": round(e2e_t, 4), "path": path,
-                       "phases": {k: round(v, 4) if isinstance(v, float) else v
-                                  for k, v in stats.items()
-                                  if k not in ("per_gpu_kernel_seconds", "culled_updates",
-                                               "culled_fraction")}}
-        if world == 1:
-            # one untimed call with the culling counters on (slower kernels)
-            cst = pkg.reconstruct_arrays(buf, g, imgs_np, mats, pkg.Options(
-                batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
-                volume_is_zero=True, count_culled=True))
-            line["culled_fraction"] = round(cst["culled_fraction"], 4)
-        del vol_h
-
-    # CPU baseline: the reference's CPU path on this box's host cores (rank 0, N=1)
+        line.update(e2e_entries(c))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cnt, cores = size_cpu_sample(cfg, args.cpu_seconds)
-            gcpu, mcpu, icpu = (g, mats[:cnt], imgs[:cnt].cpu().numpy())
-            gups, st, kind, cores = time_reference_cpu(cfg, cnt, gcpu, mcpu, icpu)
-            line["cpu_baseline"] = {
-                "value": round(gups, 4), "unit": "GUp/s", "cores": cores, "kind": kind,
-                "sample": (f"{L}^3 volume x first {cnt} of {n} projections; reconstruct_optimized "
-                           f"defaults (lanes 16, chunk 262, clip+pad); kernel "
-                           f"{st['kernel_seconds']:.2f} s (+{st.get('precompute_seconds', 0):.2f} s "
-                           f"precompute, excluded); full-basis updates")}
-            if st.get("voxel_updates"):  # the reference's own (clipped) update count
-                line["cpu_baseline"]["clipped_basis"] = {
-                    "value": round(st["voxel_updates"] / st["kernel_seconds"] / 1e9, 4),
-                    "admitted_fraction": round(st["voxel_updates"] / (L ** 3 * cnt), 4)}
-                line["cpu_baseline"]["full_basis_incl_precompute"] = round(
-                    L ** 3 * cnt / (st["kernel_seconds"] + st.get("precompute_seconds", 0.0))
-                    / 1e9, 4)
-        except Exception as e:  # the baseline is reported, never the target
-            line["cpu_baseline"] = {"value": None, "unit": "GUp/s", "cores": os.cpu_count(),
-                                    "kind": "reference", "sample": f"failed: {e}"}
+        line["cpu_baseline"] = cpu_baseline_entry(c)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def roofline_entry(c, bp_ms, nbatch, clocks):
+    """roofline of the dominant kernel (bp_kernel), per launch: algorithmic
+    FP32 ops / measured launch time vs the FP32 peak, with the gather (L1)
+    and HBM rates alongside and the ncu DRAM traffic per launch."""
+    args, cfg, L, z0, z1, nb = c.args, c.cfg, c.L, c.z0, c.z1, c.nb
+    bp_launch_ms = statistics.mean(bp_ms) / nbatch
+    updates_per_launch = (z1 - z0) * L * L * args.batch
+    peaks, peak_src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = c.torch.cuda.get_device_properties(c.dev).multi_processor_count
+    fp32_peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lane-ops/s (Tops) at max clock
+    achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
+    sm_load = clocks.get("sm_mhz") or sm_max
+    hbm_bytes = 8 * (z1 - z0) * L * L + args.batch * nb  # volume rmw + packed inputs
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        rec = json.load(open(tpath)).get(f"{cfg.name}/{args.mode}")
+        if rec and c.world == 1:
+            traffic = rec["dram_bytes_per_launch"]
+            traffic_src = f"profiles/{rec['source']} (ncu --set full, one launch)"
+    roofline = {
+        "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 3),
+        "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
+        "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(hbm_bytes),
+        "peak_basis": f"{nsm} SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, "
+                      f"{peak_src} peaks file); 34 algorithmic FP32 ops per voxel update",
+        "frac_at_load_clock": round(achieved / (nsm * 128 * sm_load * 1e6 / 1e12), 4),
+        "gups_per_launch": round(updates_per_launch / (bp_launch_ms * 1e-3) / 1e9, 2),
+        "launch_ms": round(bp_launch_ms, 4),
+        "alongside": {
+            "gather": {"achieved_GBps": round(updates_per_launch * GATHER_BYTES_PER_UPDATE /
+                                              (bp_launch_ms * 1e-3) / 1e9, 1),
+                       "peak_GBps": round(nsm * 128 * sm_max * 1e6 / 1e9, 1),
+                       "unit": "L1 B/s (128 B/clk/SM)"},
+            "hbm": {"algorithmic_GBps": round(hbm_bytes / (bp_launch_ms * 1e-3) / 1e9, 1),
+                    "peak_GBps": peaks.get("hbm_gbs")},
+        },
+    }
+    return roofline
+
+
+def secondary_entries(c):
+    """Secondary device-resident measurements (same projections, same packed
+    buffer): the other arithmetic mode on this workload, the 1024^3 volume of
+    config 3 (configs 0-3 share the scan) and the texture side number."""
+    pkg, torch, dist, dev, args, cfg = c.pkg, c.torch, c.dist, c.dev, c.args, c.cfg
+    g, mats, imgs, L, n, H, W = c.g, c.mats, c.imgs, c.L, c.n, c.H, c.W
+    z0, z1, packed, vol, err, stream, mode = c.z0, c.z1, c.packed, c.vol, c.err, c.stream, c.mode
+    rank, world = c.rank, c.world
+    from paper_1401_3615_b200 import synth
+
+    def measure(geom, mode_id, steps, slab):
+        zz0, zz1 = slab
+        LL = geom.edge_voxels
+        v2 = torch.empty(((zz1 - zz0), LL, LL), dtype=torch.float32, device=dev)
+        o2 = pkg.Options(batch=args.batch, mode=mode_id)
+
+        b2 = pkg.row_band_for_slab(geom, W, H, zz0, zz1, mats)
+
+        def st2():
+            v2.zero_()
+            pkg.pack_device_band(imgs, b2, packed, err, stream)
+            pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream,
+                                   band=b2)
+        for _ in range(2):
+            st2()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            st2()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        res = {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
+               "ms_per_step": round(ms, 3)}
+        if geom is g and mode_id != mode:
+            # full-size agreement of the two modes on the GPU (exact mode is
+            # bitwise the reference's result, see tests/test_gpu_parity.py)
+            dff = pkg.compare_volumes_device(v2, vol)
+            res["vs_exact" if mode_id == pkg.MODE_FAST else "vs_fast"] = {
+                k: dff[k] for k in ("rel_l2", "max_abs_over_range", "bitwise_different")}
+        del v2
+        return res
+
+    other = "fast" if args.mode == "exact" else "exact"
+    sec = [dict(workload=cfg.name, mode=other,
+                **measure(g, pkg.MODE_FAST if other == "fast" else pkg.MODE_EXACT,
+                          args.steps, (z0, z1)))]
+    if args.config != 3 and cfg.width == synth.CONFIGS[3].width:
+        g3 = synth.CONFIGS[3].geometry
+        if world > 1:
+            from paper_1401_3615_b200.distributed import balanced_slabs, plane_work
+            sl3 = balanced_slabs(plane_work(g3, mats, W, H), world)[rank]
+        else:
+            sl3 = (0, g3.edge_voxels)
+        sec.append(dict(workload=synth.CONFIGS[3].name, mode=args.mode,
+                        **measure(g3, mode, 3, sl3)))
+    # north_star's hardware-texture side number (not parity-exact)
+    from paper_1401_3615_b200.backproject import backproject_texture_device
+    vt = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+
+    def st_tex():
+        vt.zero_()
+        backproject_texture_device(vt, g, z0, z1, imgs, mats, stream)
+    st_tex()
+    torch.cuda.synchronize()
+    ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ta.record(stream)
+    for _ in range(3):
+        st_tex()
+    tb.record(stream)
+    torch.cuda.synchronize()
+    ms_t = ta.elapsed_time(tb) / 3
+    dtex = pkg.compare_volumes_device(vt, vol)  # vs this run's main-mode volume
+    sec.append({"workload": cfg.name, "mode": "texture (side number, not parity-exact)",
+                "value": round(L ** 3 * n / (ms_t * 1e-3) / 1e9, 3), "unit": "GUp/s",
+                "ms_per_step": round(ms_t, 3),
+                "vs_" + args.mode: {k: dtex[k] for k in ("rel_l2", "max_abs_over_range")}})
+    del vt
+    torch.cuda.empty_cache()
+    pkg.release_cached_memory()  # e.g. the texture variant's layered array
+    return sec
+
+
+
+def e2e_entries(c):
+    """e2e through the public host API: pinned host projections -> host
+    volume, H2D + kernels + D2H inside the timed region (world 1: the C ABI
+    cbb_reconstruct; world > 1: the torch.distributed driver)."""
+    pkg, torch, dist, dev, args = c.pkg, c.torch, c.dist, c.dev, c.args
+    g, mats, imgs, L, n, H, W = c.g, c.mats, c.imgs, c.L, c.n, c.H, c.W
+    z0, z1, slabs, mode, rank, world, local = c.z0, c.z1, c.slabs, c.mode, c.rank, c.world, c.local
+    total_updates, n_proj = c.total_updates, c.n
+    out = {}
+    imgs_h = imgs.cpu().pin_memory()
+    torch.cuda.empty_cache()
+    imgs_np = imgs_h.numpy()
+    # the host volume (pinned): this rank's slab planes are written by the call
+    vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
+    buf = vol_h.numpy()
+    e2e_opt = pkg.Options(batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
+                          volume_is_zero=True, slab=(z0, z1))
+    if world == 1:
+        # the drop-in C ABI: cbb_reconstruct with host buffers
+        def e2e_call():
+            buf[z0:z1] = 0.0
+            t0 = time.perf_counter()
+            st = pkg.reconstruct_arrays(buf, g, imgs_np, mats, e2e_opt)
+            return time.perf_counter() - t0, st
+        h2d = imgs_h.numel() * 4 + mats.nbytes
+        path = "cbb_reconstruct (C ABI), pinned host buffers"
+    else:
+        # one process per GPU: batch b uploaded by rank b % N, NCCL broadcast
+        from paper_1401_3615_b200.distributed import DistributedReconstructor, batch_roots
+        rec = DistributedReconstructor(g, W, H, batch=args.batch, slabs=slabs,
+                                       options=e2e_opt)
+
+        def e2e_call():
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            slab = rec.reconstruct(imgs_h, mats)
+            return time.perf_counter() - t0, {"slab_planes": int(slab.shape[0])}
+        h2d = sum(n for _, n, r in batch_roots(n_proj, args.batch, world) if r == rank) \
+            * H * W * 4 + mats.nbytes
+        path = "DistributedReconstructor: 1/N of batches uploaded per rank + NCCL broadcast"
+    e2e_call()  # warm-up
+    if dist:
+        dist.barrier()
+    e2e_s = []
+    stats = None
+    for _ in range(max(1, min(args.steps, 3))):
+        dt, stats = e2e_call()
+        e2e_s.append(dt)
+    e2e_t = statistics.median(e2e_s)
+    if dist:
+        t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    out["e2e"] = {"value": round(total_updates / e2e_t / 1e9, 3), "unit": "GUp/s",
+                  "h2d_bytes_per_step": int(h2d),
+                  "d2h_bytes_per_step": int((z1 - z0) * L * L * 4),
+                  "seconds": round(e2e_t, 4), "path": path,
+                  "phases": {k: round(v, 4) if isinstance(v, float) else v
+                             for k, v in stats.items()
+                             if k not in ("per_gpu_kernel_seconds", "culled_updates",
+                                          "culled_fraction")}}
+    if world == 1:
+        # one untimed call with the culling counters on (slower kernels)
+        cst = pkg.reconstruct_arrays(buf, g, imgs_np, mats, pkg.Options(
+            batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
+            volume_is_zero=True, count_culled=True))
+        out["culled_fraction"] = round(cst["culled_fraction"], 4)
+    del vol_h
+    return out
+
+
+def cpu_baseline_entry(c):
+    """The reference's CPU path (reconstruct_optimized from oracle/_ref) on
+    this box's host cores, on a bounded sample of the same workload."""
+    args, cfg, g, mats, imgs, L, n = c.args, c.cfg, c.g, c.mats, c.imgs, c.L, c.n
+    try:
+        cnt, cores = size_cpu_sample(cfg, args.cpu_seconds)
+        gcpu, mcpu, icpu = (g, mats[:cnt], imgs[:cnt].cpu().numpy())
+        gups, st, kind, cores = time_reference_cpu(cfg, cnt, gcpu, mcpu, icpu)
+        entry = {
+            "value": round(gups, 4), "unit": "GUp/s", "cores": cores, "kind": kind,
+            "sample": (f"{L}^3 volume x first {cnt} of {n} projections; reconstruct_optimized "
+                       f"defaults (lanes 16, chunk 262, clip+pad); kernel "
+                       f"{st['kernel_seconds']:.2f} s (+{st.get('precompute_seconds', 0):.2f} s "
+                       f"precompute, excluded); full-basis updates")}
+        if st.get("voxel_updates"):  # the reference's own (clipped) update count
+            entry["clipped_basis"] = {
+                "value": round(st["voxel_updates"] / st["kernel_seconds"] / 1e9, 4),
+                "admitted_fraction": round(st["voxel_updates"] / (L ** 3 * cnt), 4)}
+            entry["full_basis_incl_precompute"] = round(
+                L ** 3 * cnt / (st["kernel_seconds"] + st.get("precompute_seconds", 0.0))
+                / 1e9, 4)
+    except Exception as e:  # the baseline is reported, never the target
+        entry = {"value": None, "unit": "GUp/s", "cores": os.cpu_count(),
+                 "kind": "reference", "sample": f"failed: {e}"}
+    return entry
 
 
 def main():
