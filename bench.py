@@ -285,12 +285,20 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE {world} != --gpus {args.gpus}", file=sys.stderr)
+    if os.environ.get("CBB_BENCH_BACKEND", "nccl") != "nccl":
+        local %= torch.cuda.device_count()  # functional N > 1 check on fewer GPUs
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # CBB_BENCH_BACKEND=gloo only for exercising the N > 1 code path with
+        # several ranks on one GPU (functional check; its numbers mean nothing)
+        backend = os.environ.get("CBB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     cfg = synth.CONFIGS[args.config]
     mode = pkg.MODE_EXACT if args.mode == "exact" else pkg.MODE_FAST
