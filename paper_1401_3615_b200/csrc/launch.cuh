@@ -98,7 +98,8 @@ void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st)
     ++g_launches;
 }
 
-template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false>
+template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false,
+          bool SOA = false>
 void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
@@ -111,14 +112,16 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
                              ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
         grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
     }
-    bp_kernel<R, MODE, GUARD, MINB, SW, CNT><<<grid, block, 0, st>>>(args, mats);
+    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
 // Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides):
-// 0 = R 8 voxels/thread, 3 blocks/SM (default, measured best on config 2);
-// 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with super-tile order.
+// 0 = R 8 voxels/thread, 3 blocks/SM, lane pairing per mode (default, measured
+// best on config 2); 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with
+// super-tile order; 4 / 5 = the default shape with voxel-pair lanes (SOA) /
+// voxel-internal pairs in both modes.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -129,12 +132,16 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     if (GUARD) // (culling does not run in the guarded kernel: nothing to count)
         return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
     if (args.counters) // statistics requested: the counting instantiation
-        return launch_bp_r<8, MODE, GUARD, 3, 0, true>(args, mats, nz, st);
+        return launch_bp_r<8, MODE, GUARD, 3, 0, true, MODE == 0>(args, mats, nz, st);
     switch (bp_variant()) {
     case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
     case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
     case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
-    default: return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
+    case 4: return launch_bp_r<8, MODE, GUARD, 3, 0, false, true>(args, mats, nz, st);
+    case 5: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false>(args, mats, nz, st);
+    default: // measured best per mode: voxel-pair lanes (SOA) for exact, 763 vs 757
+             // GUp/s on config 2; voxel-internal pairs for fast, 873 vs 866
+        return launch_bp_r<8, MODE, GUARD, 3, 0, false, MODE == 0>(args, mats, nz, st);
     }
 }
 
