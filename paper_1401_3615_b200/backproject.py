@@ -306,8 +306,8 @@ class RowBand:
         return _lib.RowBandC(self.raw_row0, self.raw_rows, self.cell_row0, self.cell_rows)
 
     def packed_bytes(self, width: int, height: int) -> int:
-        qp, _, _ = packed_layout(width, height)
-        return qp * self.cell_rows * 16
+        qp, qr, nb = packed_layout(width, height)
+        return qp * self.cell_rows * 16 + (nb - qp * qr * 16)  # cells + metadata cell
 
 
 def row_band_for_slab(geometry: VolumeGeometry, width: int, height: int, z_begin: int,

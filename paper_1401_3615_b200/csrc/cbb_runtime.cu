@@ -111,7 +111,7 @@ cbb_status cbb_packed_layout(int32_t width, int32_t height, int32_t* qpitch, int
         if (qrows)
             *qrows = quad_rows(height);
         if (bytes)
-            *bytes = (int64_t)quad_pitch_cells(width) * quad_rows(height) * 16;
+            *bytes = (int64_t)quad_pitch_cells(width) * quad_rows(height) * 16 + kMetaBytes;
     });
 }
 

@@ -78,6 +78,10 @@ void launch_pack_band(const float* raw, int raw_row0, int raw_rows, long long ra
     dim3 grid((qp + 127) / 128, band.qn, count);
     if (band.qn <= 0 || count <= 0)
         return;
+    // zero every projection's metadata word (pack_quads only ever sets it)
+    const size_t cells_bytes = (size_t)qp * band.qn * 16;
+    CK(cudaMemset2DAsync(static_cast<char*>(packed) + cells_bytes, cells_bytes + kMetaBytes, 0,
+                         kMetaBytes, count, st));
     pack_quads<<<grid, 128, 0, st>>>(raw, W, H, raw_row0, raw_rows, raw_stride,
                                      static_cast<float4*>(packed), qp, band.q0, band.qn, err);
     CK(cudaGetLastError());
@@ -118,10 +122,10 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
 }
 
 // Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides):
-// 0 = R 8 voxels/thread, 3 blocks/SM, lane pairing per mode (default, measured
+// 0 = R 8 voxels/thread, 3 blocks/SM, voxel-internal pairs (default, measured
 // best on config 2); 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with
-// super-tile order; 4 / 5 = the default shape with voxel-pair lanes (SOA) /
-// voxel-internal pairs in both modes.
+// super-tile order; 4 = the default shape with voxel-pair lanes (SOA); 5 =
+// the default.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -132,16 +136,16 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     if (GUARD) // (culling does not run in the guarded kernel: nothing to count)
         return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
     if (args.counters) // statistics requested: the counting instantiation
-        return launch_bp_r<8, MODE, GUARD, 3, 0, true, MODE == 0>(args, mats, nz, st);
+        return launch_bp_r<8, MODE, GUARD, 3, 0, true>(args, mats, nz, st);
     switch (bp_variant()) {
     case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
     case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
     case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
     case 4: return launch_bp_r<8, MODE, GUARD, 3, 0, false, true>(args, mats, nz, st);
     case 5: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false>(args, mats, nz, st);
-    default: // measured best per mode: voxel-pair lanes (SOA) for exact, 763 vs 757
-             // GUp/s on config 2; voxel-internal pairs for fast, 873 vs 866
-        return launch_bp_r<8, MODE, GUARD, 3, 0, false, MODE == 0>(args, mats, nz, st);
+    default: // voxel-internal pairs: 784 (exact) / 873 (fast) GUp/s on config 2 vs
+             // 764 / 866 with voxel-pair lanes (variant 4)
+        return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
     }
 }
 
@@ -156,11 +160,13 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     const int qp = quad_pitch_cells(W);
     const RowBand b = band ? *band : RowBand::full(H);
     // packed projections of qn rows each; cell row q0 is the buffer's first
-    const long long proj_bytes = (long long)qp * b.qn * 16;
+    const long long proj_bytes = (long long)qp * b.qn * 16 + kMetaBytes;
     const long long band_shift = (long long)b.q0 * qp * 16;
     BpArgs args;
     args.vol = vol_slab;
     args.proj_bytes = proj_bytes;
+    // args.packed is biased by -(kMagic*16 + band_shift): undo that, skip the cells
+    args.meta_off = (long long)kMagic * 16 + band_shift + (long long)qp * b.qn * 16;
     args.L = g.edge_voxels;
     args.z_begin = z_begin;
     args.z_end = z_end;

@@ -234,7 +234,7 @@ struct Pipeline {
         if (!opt.device_ids && ng > ndev)
             fail(CBB_ERR_INVALID, "options: num_gpus %d exceeds %d visible devices", ng, ndev);
         raw_bytes_per_proj = (size_t)W * H * sizeof(float);
-        packed_bytes_per_proj = (size_t)quad_pitch_cells(W) * quad_rows(H) * 16;
+        packed_bytes_per_proj = (size_t)quad_pitch_cells(W) * quad_rows(H) * 16 + kMetaBytes;
         const int L = g.edge_voxels;
         const size_t plane = (size_t)L * L;
         for (int i = 0; i < ng; ++i) {
@@ -416,7 +416,7 @@ struct Pipeline {
     void set_bands(const double* mats, int count) {
         for (auto& w : workers) {
             w->band = band_for(*w, mats, count);
-            w->pk_bytes = (size_t)quad_pitch_cells(W) * w->band.qn * 16;
+            w->pk_bytes = (size_t)quad_pitch_cells(W) * w->band.qn * 16 + kMetaBytes;
             if (std::getenv("CBB_TRACE"))
                 std::fprintf(stderr, "cbb: device %d slab [%d, %d) rows [%d, %d) cells %d of %d\n",
                              w->device, w->z_begin, w->z_end, w->band.r0,

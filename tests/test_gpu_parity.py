@@ -570,3 +570,24 @@ def test_1024_volumes_planes_bitwise(cuda, oracle, cid, count):
         slab = np.zeros((1, L, L), np.float32)
         assert oracle.reconstruct_slab(slab, g, z0, z0 + 1, host, mats) == 0
         assert bits_equal(v[z0:z0 + 1], slab), f"config {cid} plane {z0}"
+
+
+@pytest.mark.parametrize("scale_exp", [105, -75, 0])
+def test_extreme_pixel_magnitudes_take_the_exact_fallback(cuda, oracle, scale_exp):
+    """The fast correctly-rounded weight division is proven for nonzero
+    |val| in [2^-60, 2^100]. Projections scaled by 2^105 (flagged per
+    projection by pack_quads' metadata word) or 2^-75 (caught by the kernel's
+    minimum tracking) must take the IEEE-division fallback and stay bitwise
+    equal to the reference; mixed with ordinary projections."""
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=32, num_projections=24)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=12)
+    imgs = imgs_t.numpy().astype(np.float64)
+    imgs[5] *= 2.0 ** scale_exp
+    imgs[17] *= 2.0 ** scale_exp
+    imgs = imgs.astype(np.float32)
+    assert np.all(np.isfinite(imgs))
+    ref = np.zeros((32,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    for ids in ([0], [0, 0]):
+        v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=8)
+        assert bits_equal(v, ref), (scale_exp, ids)

@@ -180,7 +180,8 @@ def test_status_names_and_layout_without_gpu():
     assert L.cbb_status_name(5) == b"geometry error"
     qp, qr, nb = pkg.packed_layout(1248, 960)
     # kPad = 48 cells of zero margin on each side (rows padded to 8 cells)
-    assert qp % 8 == 0 and qp >= 1248 + 96 and qr == 960 + 96 and nb == qp * qr * 16
+    # plus one 16-byte metadata cell per projection
+    assert qp % 8 == 0 and qp >= 1248 + 96 and qr == 960 + 96 and nb == qp * qr * 16 + 16
     with pytest.raises(pkg.ValidationError):
         pkg.packed_layout(0, 10)
 
