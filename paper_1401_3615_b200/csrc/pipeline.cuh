@@ -148,14 +148,14 @@ struct Pipeline {
     // fewest planes that holds ~kTailFrac of the slab's estimated work. Work
     // per group = fraction of sampled (x, y, projection) positions that land
     // on the detector (the rest is culled warp by warp) + a fixed overhead,
-    // sampled on a 16 x 16 grid at the group's centre plane for up to 8 of
+    // sampled on a 12 x 12 grid at the group's centre plane for up to 4 of
     // the given projections. A dense tail keeps its D2H short while its
     // compute hides the head's D2H.
     void choose_tails(const double* mats, int n) {
         double frac = 0.12;
         if (const char* e = std::getenv("CBB_TAIL_FRAC"))
             frac = std::atof(e);
-        const int L = g.edge_voxels, S = 16, NP = std::min(n, 8);
+        const int L = g.edge_voxels, S = 12, NP = std::min(n, 4);
         for (auto& w : workers) {
             std::vector<double> gw;
             std::vector<int> gz;
