@@ -309,14 +309,6 @@ struct Pipeline {
     // corresponding h2d_done events complete (wait_slot).
     void issue(const float* src, const double* mats, int n) {
         const size_t bytes = raw_bytes_per_proj * n;
-        if (resident && submitted == 0) {
-            const auto t0 = std::chrono::steady_clock::now();
-            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
-            if (std::getenv("CBB_TRACE"))
-                std::fprintf(stderr, "cbb: choose_tails %.2f ms\n",
-                             std::chrono::duration<double, std::milli>(
-                                 std::chrono::steady_clock::now() - t0).count());
-        }
         // Batch k is uploaded once, by the root worker k mod G, and each
         // other worker copies its row band from the root's raw slot (peer
         // copy over NVLink; a plain device copy when both are one device).
@@ -355,6 +347,16 @@ struct Pipeline {
             CK(cudaEventRecord(w->h2d_done[slot], w->copy));
             CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
             start_timing(*w);
+        }
+        // the tails are needed by the first back-projection only: choose them
+        // once the first upload is already on its way
+        if (resident && submitted == 0) {
+            const auto t0 = std::chrono::steady_clock::now();
+            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: choose_tails %.2f ms\n",
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
         }
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
