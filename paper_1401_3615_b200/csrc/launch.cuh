@@ -191,10 +191,12 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     const float Of = (float)g.origin_mm, MMf = (float)g.voxel_mm;
     const double cxy = min_nonzero_coord(Of, MMf, 0, g.edge_voxels);
     const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, z_begin, z_end)};
+    // CBB_FORCE_GUARDED (tests): run every batch through the guarded kernel
+    const bool force_guarded = std::getenv("CBB_FORCE_GUARDED") != nullptr && err;
     for (int first = 0; first < count; first += opt.batch) {
         const int n = std::min(opt.batch, count - first);
         BpMats m;
-        bool safe = true;
+        bool safe = !force_guarded;
         for (int p = 0; p < n; ++p) {
             const double* a = mats + 12 * (size_t)(first + p);
             store_matrix(m.a[p], a);

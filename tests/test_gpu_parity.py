@@ -591,3 +591,17 @@ def test_extreme_pixel_magnitudes_take_the_exact_fallback(cuda, oracle, scale_ex
     for ids in ([0], [0, 0]):
         v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=8)
         assert bits_equal(v, ref), (scale_exp, ids)
+
+
+@pytest.mark.parametrize("name", ["mini_c0.npz", "orthographic.npz"])
+def test_guarded_kernel_equals_fast_path(cuda, monkeypatch, name):
+    """proj/tests/test_kernel_ref.cpp:51-65 restated for the two kernels: the
+    guarded kernel (scalar IEEE divisions, reference guards; used when the
+    host cannot prove a batch safe) and the unguarded fast path give the
+    same bits, both equal to the reference fixture."""
+    g, mats, imgs, vol0, expected = load_golden(name)
+    v_fast, st_fast = gpu_reconstruct(g, mats, imgs, vol0)
+    monkeypatch.setenv("CBB_FORCE_GUARDED", "1")
+    v_guard, st_guard = gpu_reconstruct(g, mats, imgs, vol0)
+    assert st_fast["guarded_batches"] == 0 and st_guard["guarded_batches"] > 0
+    assert bits_equal(v_fast, expected) and bits_equal(v_guard, expected)

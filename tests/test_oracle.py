@@ -166,3 +166,18 @@ def test_trajectory_equals_reference(oracle):
     for cfg in (TrajectoryConfig(17, 750.0, 1200.0, 1248, 960, 0.32, math.radians(200.0)),
                 TrajectoryConfig(5, 1000.0, 1500.0, 1536, 1536, 0.2)):
         assert np.array_equal(make_circular_trajectory(cfg), oracle.ref_trajectory(cfg))
+
+
+@needs_ref
+def test_reference_optimized_degenerate_options_are_the_reference(oracle):
+    """proj/tests/test_kernel_opt.cpp:384-398 restated: reconstruct_optimized
+    with lanes 1, one worker, no clip, no pad is bitwise reconstruct_reference
+    (the CPU baseline's code path, run here from oracle/_ref)."""
+    g, mats, imgs = oracle.golden_case()
+    a = np.zeros((64,) * 3, np.float32)
+    b = np.zeros((64,) * 3, np.float32)
+    assert oracle.ref_reconstruct_reference(a, g, imgs, mats) == 0
+    st = oracle.ref_reconstruct_optimized(b, g, imgs, mats, lanes=1, chunk=262, workers=1,
+                                          use_clip=False, use_pad=False)
+    assert st["status"] == 0
+    assert bits_equal(a, b)
