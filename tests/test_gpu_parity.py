@@ -605,3 +605,40 @@ def test_guarded_kernel_equals_fast_path(cuda, monkeypatch, name):
     v_guard, st_guard = gpu_reconstruct(g, mats, imgs, vol0)
     assert st_fast["guarded_batches"] == 0 and st_guard["guarded_batches"] > 0
     assert bits_equal(v_fast, expected) and bits_equal(v_guard, expected)
+
+
+def test_affine_field_reproduced_and_within_tap_hull(cuda, oracle):
+    """proj/tests/test_kernel_ref.cpp:67-115 restated on the GPU path: with an
+    affine projection field (the golden 'ramp' ix + 2 iy), voxels that project
+    inside the detector in every view get exactly the field's values, so the
+    volume matches a float64 evaluation of sum_p (ix + 2 iy) / w^2 to 1e-4
+    relative there; and a single projection's update lies within the hull of
+    its four taps scaled by 1/w^2."""
+    g, mats, imgs = oracle.golden_case()
+    v, _ = gpu_reconstruct(g, mats, imgs, np.zeros((64,) * 3, np.float32))
+    L = g.edge_voxels
+    idx = g.origin_mm + np.arange(L) * g.voxel_mm
+    Z, Y, X = np.meshgrid(idx, idx, idx, indexing="ij")
+    hom = np.stack([X.ravel(), Y.ravel(), Z.ravel(), np.ones(X.size)])
+    acc = np.zeros(X.size)
+    inside = np.ones(X.size, bool)
+    for a in mats:
+        u, vv, w = a.reshape(4, 3).T @ hom
+        ix, iy = u / w, vv / w
+        inside &= (ix > 0.01) & (iy > 0.01) & (ix < 158.99) & (iy < 158.99)
+        acc += (ix + 2.0 * iy) / (w * w)
+    assert inside.sum() > 0.2 * X.size
+    got = v.ravel().astype(np.float64)[inside]
+    err = np.abs(got - acc[inside]).max() / np.abs(acc[inside]).max()
+    assert err < 1e-4, err
+    # one projection: the update at every interior voxel lies within its taps' hull
+    one, _ = gpu_reconstruct(g, mats[:1], imgs[:1], np.zeros((64,) * 3, np.float32))
+    u, vv, w = mats[0].reshape(4, 3).T @ hom
+    fx, fy = u / w, vv / w
+    ok = (fx > 0.01) & (fy > 0.01) & (fx < 158.99) & (fy < 158.99)
+    ix, iy = np.floor(fx), np.floor(fy)
+    lo = (ix + 2.0 * iy) / (w * w)
+    hi = (ix + 1 + 2.0 * (iy + 1)) / (w * w)
+    o = one.ravel().astype(np.float64)
+    assert np.all(o[ok] >= lo[ok] * (1 - 1e-5) - 1e-6)
+    assert np.all(o[ok] <= hi[ok] * (1 + 1e-5) + 1e-6)
