@@ -5,7 +5,7 @@
 // batch and the launches of the sm_100a kernels in bp_kernels.cuh
 // (launch.cuh), buffer caches (memory.cuh) and the staging pipeline
 // (pipeline.cuh):
-//   host projections --(pinned, double-buffered cudaMemcpyAsync on a copy
+//   host projections --(pinned, ring-buffered cudaMemcpyAsync on a copy
 //   stream)--> raw ring slot --(pack_quads on the compute stream)--> packed
 //   ring slot --(bp_kernel, matrices as kernel parameters = constant bank)-->
 //   register partial sums --> volume slab in HBM.

@@ -8,6 +8,11 @@
 
 namespace cbb {
 
+// Ring slots per device (raw, packed, pinned host staging). Two suffice: a
+// third did not speed up pageable sources (measured 97.6 vs 96-97 ms on
+// config 2), whose host copies contend with the H2D DMA for host memory.
+constexpr int kSlots = 2;
+
 // ---------------------------------------------------------------------------
 // Per-device worker: slab volume, raw/packed double buffers, streams, events.
 // ---------------------------------------------------------------------------
@@ -16,11 +21,11 @@ struct Worker {
     int device = 0;
     int z_begin = 0, z_end = 0;
     float* d_vol = nullptr;
-    float* d_raw[2] = {nullptr, nullptr};
-    void* d_packed[2] = {nullptr, nullptr};
+    float* d_raw[kSlots] = {};
+    void* d_packed[kSlots] = {};
     int* d_err = nullptr;
     cudaStream_t copy = nullptr, compute = nullptr;
-    cudaEvent_t h2d_done[2] = {}, raw_free[2] = {};
+    cudaEvent_t h2d_done[kSlots] = {}, raw_free[kSlots] = {};
     cudaEvent_t k_beg = nullptr, k_end = nullptr, c_beg = nullptr, c_end = nullptr;
     double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
     uint64_t guarded = 0;
@@ -36,7 +41,7 @@ struct Worker {
     // detector rows this worker holds / packs (RowBand::full unless set_bands)
     RowBand band;
     size_t pk_bytes = 0;               // packed bytes per projection (band rows)
-    cudaEvent_t src_ready[2] = {};     // as root: raw slot filtered, peers may copy
+    cudaEvent_t src_ready[kSlots] = {}; // as root: raw slot filtered, peers may copy
     cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
     unsigned long long* d_counters = nullptr; // kCounterSlots culled-update counters
     bool count_culled = false;
@@ -49,14 +54,15 @@ struct Worker {
         cudaStreamSynchronize(compute);
         auto& pool = DevicePool::get();
         pool.release(device, d_vol);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kSlots; ++i) {
             pool.release(device, d_raw[i]);
             pool.release(device, d_packed[i]);
             cudaEventDestroy(h2d_done[i]);
             cudaEventDestroy(raw_free[i]);
             cudaEventDestroy(src_ready[i]);
-            cudaEventDestroy(xfer_ev[i]);
         }
+        for (auto e : xfer_ev)
+            cudaEventDestroy(e);
         pool.release(device, d_err);
         pool.release(device, d_counters);
         pool.release(device, d_packed_all);
@@ -84,7 +90,7 @@ struct Pipeline {
     int W = 0, H = 0;
     cbb_options opt{};
     std::vector<std::unique_ptr<Worker>> workers;
-    float* h_stage[2] = {nullptr, nullptr}; // pinned staging (batch x H x W)
+    float* h_stage[kSlots] = {};            // pinned staging (batch x H x W)
     ChunkedXfer xfer;                       // volume up/download for pageable buffers
     int stage_fill = 0;                     // projections staged in the current slot
     int slot = 0;                           // current staging / ring slot
@@ -210,8 +216,8 @@ struct Pipeline {
 
     ~Pipeline() {
         workers.clear();
-        for (int i = 0; i < 2; ++i)
-            HostPool::get().release(h_stage[i]);
+        for (auto h : h_stage)
+            HostPool::get().release(h);
     }
 
     void init(const cbb_volume_geometry& geom, int width, int height, const cbb_options& o,
@@ -247,15 +253,16 @@ struct Pipeline {
             CK(cudaSetDevice(w->device));
             CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
             CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));
-            for (int s = 0; s < 2; ++s) {
+            for (int s = 0; s < kSlots; ++s) {
                 CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->src_ready[s], cudaEventDisableTiming));
-                CK(cudaEventCreateWithFlags(&w->xfer_ev[s], cudaEventDisableTiming));
                 w->d_raw[s] = static_cast<float*>(
                     DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
                 w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
             }
+            for (auto& e : w->xfer_ev)
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             w->band = RowBand::full(H);
             w->pk_bytes = packed_bytes_per_proj;
             CK(cudaEventCreate(&w->k_beg));
@@ -380,7 +387,7 @@ struct Pipeline {
         if (resident)
             std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
         submitted += n;
-        slot ^= 1;
+        slot = (slot + 1) % kSlots;
     }
 
     void start_timing(Worker& w) {
@@ -450,7 +457,7 @@ struct Pipeline {
 
     // Pinned staging for pageable sources, allocated on first use only.
     void ensure_staging() {
-        for (int s = 0; s < 2; ++s)
+        for (int s = 0; s < kSlots; ++s)
             if (!h_stage[s])
                 h_stage[s] = HostPool::get().alloc(raw_bytes_per_proj * opt.batch);
     }
@@ -483,7 +490,7 @@ struct Pipeline {
 
     // Whole-stack submission straight from the caller's buffer: pinned
     // buffers are copied asynchronously in place, pageable ones are staged
-    // through the pinned double buffer.
+    // through the pinned staging ring (kSlots buffers).
     // First submission of a stack whose matrices are all known: row bands,
     // resident mode, tail estimate.
     void begin_stack(const double* mats, int count) {
