@@ -103,7 +103,7 @@ void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st)
 }
 
 template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false,
-          bool SOA = false>
+          bool SOA = false, int TW = 8>
 void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
@@ -116,7 +116,7 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
                              ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
         grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
     }
-    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA><<<grid, block, 0, st>>>(args, mats);
+    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA, TW><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -125,7 +125,8 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
 // 0 = R 8 voxels/thread, 3 blocks/SM, voxel-internal pairs (default, measured
 // best on config 2); 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with
 // super-tile order; 4 = the default shape with voxel-pair lanes (SOA); 5 =
-// the default.
+// the default; 6 / 7 / 8 = warp tiles of 16x2 / 4x8 / 32x1 voxels instead of
+// 8x4 (783 / 784 / 774 vs 784 GUp/s exact on config 2).
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -143,6 +144,9 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
     case 4: return launch_bp_r<8, MODE, GUARD, 3, 0, false, true>(args, mats, nz, st);
     case 5: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false>(args, mats, nz, st);
+    case 6: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 16>(args, mats, nz, st);
+    case 7: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 4>(args, mats, nz, st);
+    case 8: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 32>(args, mats, nz, st);
     default: // voxel-internal pairs: 784 (exact) / 873 (fast) GUp/s on config 2 vs
              // 764 / 866 with voxel-pair lanes (variant 4)
         return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
