@@ -75,7 +75,7 @@ void launch_pack_band(const float* raw, int raw_row0, int raw_rows, long long ra
                       int H, int count, void* packed, const RowBand& band, cudaStream_t st,
                       int* err) {
     const int qp = quad_pitch_cells(W);
-    dim3 grid((qp + 127) / 128, band.qn, count);
+    dim3 grid((qp + 127) / 128, (band.qn + kPackRows - 1) / kPackRows, count);
     if (band.qn <= 0 || count <= 0)
         return;
     // zero every projection's metadata word (pack_quads only ever sets it)
