@@ -78,7 +78,7 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
-def _image(img, width=None, height=None) -> np.ndarray:
+def _image(img) -> np.ndarray:
     a = np.ascontiguousarray(img, dtype=np.float32)
     if a.ndim != 2:
         raise ValidationError("ProjectionImage: expected a 2-D (height, width) array")

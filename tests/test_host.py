@@ -4,7 +4,6 @@ import ctypes
 import math
 import os
 import re
-import struct
 
 import numpy as np
 import pytest
