@@ -32,6 +32,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -414,6 +415,7 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, cons
                            int32_t width, int32_t height, int32_t count, const double* mats,
                            const cbb_options* options, cbb_run_stats* stats) {
     return guarded([&] {
+        NvtxRange range("cbb_reconstruct");
         const auto t0 = std::chrono::steady_clock::now();
         if (!vol || !imgs || !mats)
             fail(CBB_ERR_INVALID, "cbb_reconstruct: null argument");
@@ -456,6 +458,7 @@ cbb_status cbb_reconstruct_images(float* vol, const cbb_volume_geometry* geometr
                                   int32_t count, const double* mats,
                                   const cbb_options* options, cbb_run_stats* stats) {
     return guarded([&] {
+        NvtxRange range("cbb_reconstruct_images");
         const auto t0 = std::chrono::steady_clock::now();
         if (!vol || !imgs || !mats)
             fail(CBB_ERR_INVALID, "cbb_reconstruct_images: null argument");
@@ -565,6 +568,7 @@ cbb_status cbb_stack_file_query(const char* path, cbb_stack_file_info* out) {
 cbb_status cbb_reconstruct_file(float* vol, const char* path, const cbb_options* options,
                                 cbb_run_stats* stats) {
     return guarded([&] {
+        NvtxRange range("cbb_reconstruct_file");
         const auto t0 = std::chrono::steady_clock::now();
         if (!vol || !path)
             fail(CBB_ERR_INVALID, "cbb_reconstruct_file: null argument");

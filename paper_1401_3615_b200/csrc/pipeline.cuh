@@ -315,6 +315,7 @@ struct Pipeline {
     // to every worker. The caller guarantees src stays valid until the
     // corresponding h2d_done events complete (wait_slot).
     void issue(const float* src, const double* mats, int n) {
+        NvtxRange range("cbb batch");
         const size_t bytes = raw_bytes_per_proj * n;
         // Batch k is uploaded once, by the root worker k mod G, and each
         // other worker copies its row band from the root's raw slot (peer
@@ -496,6 +497,7 @@ struct Pipeline {
     void begin_stack(const double* mats, int count) {
         if (submitted != 0)
             return;
+        NvtxRange range("cbb setup (bands, resident)");
         const auto t0 = std::chrono::steady_clock::now();
         set_bands(mats, count);
         enable_resident(count);
@@ -672,6 +674,7 @@ struct Pipeline {
 
     // Waits for all work, checks the error flags, downloads slabs into vol_out.
     void finish(float* vol_out) {
+        NvtxRange range("cbb finish");
         flush();
         const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
         if (resident) {

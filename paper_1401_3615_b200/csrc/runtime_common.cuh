@@ -28,6 +28,15 @@ thread_local uint64_t g_launches = 0;
     throw Error(s, buf);
 }
 
+// NVTX range for the lifetime of the object (host phases in nsys / ncu
+// timelines: call, batch issue, finish); no cost without a profiler.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void check_cuda(cudaError_t e, const char* what) {
     if (e == cudaSuccess)
         return;
