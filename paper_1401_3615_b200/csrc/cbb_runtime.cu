@@ -433,7 +433,7 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, cons
         double t_init = 0, t_sub = 0, t_fin = 0;
         {
             Pipeline pipe;
-            pipe.init(*geometry, width, height, opt, vol);
+            pipe.init(*geometry, width, height, opt, vol, mats, count);
             t_init = ms();
             pipe.submit_stack(imgs, mats, count);
             t_sub = ms();
@@ -473,7 +473,7 @@ cbb_status cbb_reconstruct_images(float* vol, const cbb_volume_geometry* geometr
         const cbb_options opt = resolve_options(options);
         {
             Pipeline pipe;
-            pipe.init(*geometry, width, height, opt, vol);
+            pipe.init(*geometry, width, height, opt, vol, mats, count);
             pipe.submit_images(imgs, mats, count);
             pipe.finish(vol);
             pipe.fill_stats(stats, 0.0);

@@ -85,6 +85,60 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
     return ms * 1e-3;
 }
 
+// Estimated back-projection work of the 8-plane groups of [z0, z1) (group g
+// starts at plane z0 + 8g): planes x (fraction of sampled (x, y, projection)
+// positions that land on the detector -- warp culling skips the rest -- +
+// a fixed overhead), sampled on a 12 x 12 grid at the group's centre plane for
+// up to 4 of the n projections.
+std::vector<double> group_work(const cbb_volume_geometry& g, int W, int H, int z0, int z1,
+                               const double* mats, int n) {
+    const int L = g.edge_voxels, S = 12, NP = std::min(n, 4);
+    std::vector<double> gw;
+    for (int z = z0; z < z1; z += 8) {
+        const int pz = std::min(8, z1 - z);
+        const double zc = g.origin_mm + (z + (pz - 1) * 0.5) * g.voxel_mm;
+        int on = 0;
+        for (int k = 0; k < NP; ++k) {
+            const double* a = mats + 12 * (size_t)((long long)k * n / NP);
+            for (int j = 0; j < S; ++j)
+                for (int i = 0; i < S; ++i) {
+                    const double x = g.origin_mm + (L - 1) * (i / (S - 1.0)) * g.voxel_mm;
+                    const double y = g.origin_mm + (L - 1) * (j / (S - 1.0)) * g.voxel_mm;
+                    const double u = a[0] * x + a[3] * y + a[6] * zc + a[9];
+                    const double v = a[1] * x + a[4] * y + a[7] * zc + a[10];
+                    const double ww = a[2] * x + a[5] * y + a[8] * zc + a[11];
+                    const double ix = u / ww, iy = v / ww;
+                    on += ix > -2 && ix < W && iy > -2 && iy < H;
+                }
+        }
+        gw.push_back(pz * ((double)on / (NP * S * S) + 0.05));
+    }
+    return gw;
+}
+
+// ng contiguous slabs of [s0, s1) with near-equal estimated work (the
+// single-process counterpart of distributed.py's balanced_slabs); each gets
+// at least one plane.
+std::vector<int> balanced_bounds(const cbb_volume_geometry& g, int W, int H, int s0, int s1,
+                                 int ng, const double* mats, int n) {
+    const std::vector<double> gw = group_work(g, W, H, s0, s1, mats, n);
+    std::vector<double> cum(1, 0.0); // per-plane prefix sums
+    for (int z = s0; z < s1; ++z) {
+        const int k = (z - s0) / 8;
+        const int pz = std::min(8, s1 - (s0 + 8 * k));
+        cum.push_back(cum.back() + gw[k] / pz);
+    }
+    std::vector<int> b(1, s0);
+    for (int r = 1; r < ng; ++r) {
+        const double target = cum.back() * r / ng;
+        int z = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        z = std::max(b.back() - s0 + 1, std::min(z, (s1 - s0) - (ng - r)));
+        b.push_back(s0 + z);
+    }
+    b.push_back(s1);
+    return b;
+}
+
 struct Pipeline {
     cbb_volume_geometry g{};
     int W = 0, H = 0;
@@ -161,30 +215,11 @@ struct Pipeline {
         double frac = 0.12;
         if (const char* e = std::getenv("CBB_TAIL_FRAC"))
             frac = std::atof(e);
-        const int L = g.edge_voxels, S = 12, NP = std::min(n, 4);
         for (auto& w : workers) {
-            std::vector<double> gw;
+            const std::vector<double> gw = group_work(g, W, H, w->z_begin, w->z_end, mats, n);
             std::vector<int> gz;
-            for (int z = w->z_begin; z < w->z_end; z += 8) {
-                const int pz = std::min(8, w->z_end - z);
-                const double zc = g.origin_mm + (z + (pz - 1) * 0.5) * g.voxel_mm;
-                int on = 0;
-                for (int k = 0; k < NP; ++k) {
-                    const double* a = mats + 12 * (size_t)((long long)k * n / NP);
-                    for (int j = 0; j < S; ++j)
-                        for (int i = 0; i < S; ++i) {
-                            const double x = g.origin_mm + (L - 1) * (i / (S - 1.0)) * g.voxel_mm;
-                            const double y = g.origin_mm + (L - 1) * (j / (S - 1.0)) * g.voxel_mm;
-                            const double u = a[0] * x + a[3] * y + a[6] * zc + a[9];
-                            const double v = a[1] * x + a[4] * y + a[7] * zc + a[10];
-                            const double ww = a[2] * x + a[5] * y + a[8] * zc + a[11];
-                            const double ix = u / ww, iy = v / ww;
-                            on += ix > -2 && ix < W && iy > -2 && iy < H;
-                        }
-                }
-                gw.push_back(pz * ((double)on / (NP * S * S) + 0.05));
+            for (int z = w->z_begin; z < w->z_end; z += 8)
                 gz.push_back(z);
-            }
             gz.push_back(w->z_end);
             const int G = (int)gw.size();
             double total = 0.0;
@@ -220,8 +255,11 @@ struct Pipeline {
             HostPool::get().release(h);
     }
 
+    // mats/nmats (nullable): the whole stack's matrices; with several devices
+    // and culling on, the slabs are then balanced by estimated work instead
+    // of equal plane counts.
     void init(const cbb_volume_geometry& geom, int width, int height, const cbb_options& o,
-              const float* initial_volume) {
+              const float* initial_volume, const double* mats = nullptr, int nmats = 0) {
         g = geom;
         W = width;
         H = height;
@@ -243,13 +281,17 @@ struct Pipeline {
         packed_bytes_per_proj = (size_t)quad_pitch_cells(W) * quad_rows(H) * 16 + kMetaBytes;
         const int L = g.edge_voxels;
         const size_t plane = (size_t)L * L;
+        std::vector<int> bounds;
+        if (mats && nmats > 0 && ng > 1 && opt.cull)
+            bounds = balanced_bounds(g, W, H, s0, s1, ng, mats, nmats);
         for (int i = 0; i < ng; ++i) {
             auto w = std::make_unique<Worker>();
             w->device = opt.device_ids ? opt.device_ids[i] : i;
             if (w->device < 0 || w->device >= ndev)
                 fail(CBB_ERR_INVALID, "options: device id %d not visible", w->device);
-            w->z_begin = s0 + (int)((long long)(s1 - s0) * i / ng);
-            w->z_end = s0 + (int)((long long)(s1 - s0) * (i + 1) / ng);
+            w->z_begin = bounds.empty() ? s0 + (int)((long long)(s1 - s0) * i / ng) : bounds[i];
+            w->z_end = bounds.empty() ? s0 + (int)((long long)(s1 - s0) * (i + 1) / ng)
+                                      : bounds[i + 1];
             CK(cudaSetDevice(w->device));
             CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
             CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));

@@ -642,3 +642,26 @@ def test_affine_field_reproduced_and_within_tap_hull(cuda, oracle):
     o = one.ravel().astype(np.float64)
     assert np.all(o[ok] >= lo[ok] * (1 - 1e-5) - 1e-6)
     assert np.all(o[ok] <= hi[ok] * (1 + 1e-5) + 1e-6)
+
+
+def test_single_process_slabs_are_work_balanced(cuda, oracle, monkeypatch, capfd):
+    """cbb_reconstruct with 4 workers and the whole stack known: the z-slabs
+    are split by estimated (non-culled) work, so the outer slabs, whose planes
+    leave the field of view, hold more planes; the result stays bitwise."""
+    import re
+
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=30)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=15)
+    imgs = imgs_t.numpy()
+    ref = np.zeros((64,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    monkeypatch.setenv("CBB_TRACE", "1")
+    capfd.readouterr()
+    v, _ = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=[0, 0, 0, 0])
+    err = capfd.readouterr().err
+    slabs = sorted({(int(a), int(b)) for a, b in re.findall(r"slab \[(\d+), (\d+)\) rows", err)})
+    assert len(slabs) == 4 and slabs[0][0] == 0 and slabs[-1][1] == 64
+    assert all(slabs[i][1] == slabs[i + 1][0] for i in range(3))
+    sizes = [b - a for a, b in slabs]
+    assert sizes[0] > sizes[1] and sizes[3] > sizes[2], sizes
+    assert bits_equal(v, ref)
