@@ -665,3 +665,22 @@ def test_single_process_slabs_are_work_balanced(cuda, oracle, monkeypatch, capfd
     sizes = [b - a for a, b in slabs]
     assert sizes[0] > sizes[1] and sizes[3] > sizes[2], sizes
     assert bits_equal(v, ref)
+
+
+def test_resume_from_partial_volume_is_bitwise(cuda):
+    """Checkpoint / resume: reconstruct the first part of a
+    stack, save the volume (CBPV round trip), continue with the rest on top
+    of it -- bitwise the single-call result, as in the reference's additivity
+    test (proj/tests/test_kernel_ref.cpp:190-222)."""
+    import tempfile
+
+    g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
+    k = len(mats) // 3
+    part = pkg.Volume(g, vol0.copy())
+    pkg.reconstruct(part, pkg.ProjectionStack(g, mats[:k], imgs[:k]))
+    with tempfile.TemporaryDirectory() as d:
+        path = d + "/part.cbpv"
+        pkg.write_volume(path, part)
+        resumed = pkg.read_volume(path)
+    pkg.reconstruct(resumed, pkg.ProjectionStack(g, mats[k:], imgs[k:]))
+    assert bits_equal(resumed.voxels, expected)
