@@ -151,6 +151,7 @@ struct Pipeline {
     std::vector<double> stage_mats;         // matrices of the staged batch
     uint64_t submitted = 0;
     uint64_t nbatch = 0;   // batches issued (root = nbatch mod workers)
+    bool peer_pack = false; // non-root workers pack from the root's raw slot directly
     size_t raw_bytes_per_proj = 0;
     size_t packed_bytes_per_proj = 0;
     bool resident = false;         // see Worker::d_packed_all
@@ -332,13 +333,19 @@ struct Pipeline {
             workers.push_back(std::move(w));
         }
         stage_mats.assign(12 * (size_t)opt.batch, 0.0);
-        // band copies go straight over NVLink where the devices allow it
+        // peer access between every pair of devices: band reads go straight
+        // over NVLink; without it for some pair, band copies are staged
+        peer_pack = !std::getenv("CBB_NO_PEER_PACK");
         for (auto& a : workers)
             for (auto& b : workers) {
                 int can = 0;
-                if (a->device == b->device ||
-                    cudaDeviceCanAccessPeer(&can, b->device, a->device) != cudaSuccess || !can)
+                if (a->device == b->device)
                     continue;
+                if (cudaDeviceCanAccessPeer(&can, b->device, a->device) != cudaSuccess || !can) {
+                    cudaGetLastError();
+                    peer_pack = false;
+                    continue;
+                }
                 CK(cudaSetDevice(b->device));
                 const cudaError_t e = cudaDeviceEnablePeerAccess(a->device, 0);
                 if (e == cudaErrorPeerAccessAlreadyEnabled)
@@ -359,19 +366,24 @@ struct Pipeline {
     void issue(const float* src, const double* mats, int n) {
         NvtxRange range("cbb batch");
         const size_t bytes = raw_bytes_per_proj * n;
-        // Batch k is uploaded once, by the root worker k mod G, and each
-        // other worker copies its row band from the root's raw slot (peer
-        // copy over NVLink; a plain device copy when both are one device).
+        // Batch k is uploaded once, by the root worker k mod G. Each other
+        // worker packs its row band straight out of the root's raw slot over
+        // peer memory (pack_quads' loads cross NVLink: the transfer and the
+        // layout transform are one kernel), or, without peer access, first
+        // copies the band rows (cudaMemcpy3DPeerAsync) and packs locally.
         const int G = (int)workers.size();
         Worker& root = *workers[nbatch % G];
         // raw[slot] of worker w may still be read by its own pack of batch
-        // k-2 and, if w was that batch's root, by the other workers' band copies
+        // k-kSlots and, if w was that batch's root, by the other workers'
+        // band copies (h2d_done) or peer packs (raw_free)
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
             for (auto& o : workers)
-                if (o != w)
+                if (o != w) {
                     CK(cudaStreamWaitEvent(w->copy, o->h2d_done[slot], 0));
+                    CK(cudaStreamWaitEvent(w->copy, o->raw_free[slot], 0));
+                }
         }
         CK(cudaSetDevice(root.device));
         CK(cudaMemcpyAsync(root.d_raw[slot], src, bytes, cudaMemcpyHostToDevice, root.copy));
@@ -392,10 +404,14 @@ struct Pipeline {
             if (w.get() == &root)
                 continue;
             CK(cudaSetDevice(w->device));
-            CK(cudaStreamWaitEvent(w->copy, ready, 0));
-            copy_band(root, *w, slot, n);
-            CK(cudaEventRecord(w->h2d_done[slot], w->copy));
-            CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
+            if (peer_pack) {
+                CK(cudaStreamWaitEvent(w->compute, ready, 0));
+            } else {
+                CK(cudaStreamWaitEvent(w->copy, ready, 0));
+                copy_band(root, *w, slot, n);
+                CK(cudaEventRecord(w->h2d_done[slot], w->copy));
+                CK(cudaStreamWaitEvent(w->compute, w->h2d_done[slot], 0));
+            }
             start_timing(*w);
         }
         // the tails are needed by the first back-projection only: choose them
@@ -415,6 +431,9 @@ struct Pipeline {
             if (w.get() == &root)
                 launch_pack_band(w->d_raw[slot], 0, H, (long long)W * H, W, H, n, packed, w->band,
                                  w->compute, w->d_err);
+            else if (peer_pack) // the root's full raw slot, read over peer memory
+                launch_pack_band(root.d_raw[slot], 0, H, (long long)W * H, W, H, n, packed,
+                                 w->band, w->compute, w->d_err);
             else
                 launch_pack_band(w->d_raw[slot], w->band.r0, w->band.rn,
                                  (long long)w->band.rn * W, W, H, n, packed, w->band, w->compute,

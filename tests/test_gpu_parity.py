@@ -260,13 +260,18 @@ def _bands_from_trace(err: str):
     return out
 
 
-@pytest.mark.parametrize("ids,filt", [([0, 0, 0, 0], False), ([0, 0, 0], True),
-                                      ([0, 0, 0, 0, 0], True)])
-def test_row_bands_and_rotating_roots_bitwise(cuda, oracle, monkeypatch, capfd, ids, filt):
+@pytest.mark.parametrize("ids,filt,peer", [([0, 0, 0, 0], False, True), ([0, 0, 0], True, True),
+                                           ([0, 0, 0, 0, 0], True, True),
+                                           ([0, 0, 0, 0], False, False),
+                                           ([0, 0, 0], True, False)])
+def test_row_bands_and_rotating_roots_bitwise(cuda, oracle, monkeypatch, capfd, ids, filt, peer):
     """Several slab workers: batch k is uploaded once by worker k mod G and the
-    others copy only the detector rows their slab projects onto (strided peer
-    copy; here all workers share one device). Bitwise equal to the oracle,
-    with and without the in-pipeline ramp filter (then vs one worker)."""
+    others pack only the detector rows their slab projects onto, reading the
+    root's slot over peer memory (peer) or after a strided band copy (here all
+    workers share one device). Bitwise equal to the oracle, with and without
+    the in-pipeline ramp filter (then vs one worker)."""
+    if not peer:
+        monkeypatch.setenv("CBB_NO_PEER_PACK", "1")
     cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=45)
     g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=15)
     imgs = imgs_t.numpy()
