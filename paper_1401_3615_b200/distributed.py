@@ -153,7 +153,7 @@ class DistributedReconstructor:
 
     def __init__(self, geometry: VolumeGeometry, width: int, height: int, batch: int = 32,
                  slabs: Optional[Sequence[tuple]] = None, group=None, device=None,
-                 hooks: Optional[Hooks] = None, options=None):
+                 hooks: Optional[Hooks] = None, options=None, slots: Optional[int] = None):
         import torch
         import torch.distributed as dist
 
@@ -174,10 +174,16 @@ class DistributedReconstructor:
         self.cuda = self.device.type == "cuda"
         self.hooks = hooks or cuda_hooks(geometry, width, height, options)
         nb = self.hooks.packed_bytes
+        # raw slots in flight: world + 1, so the uploads of the next `world`
+        # batches (each by a different rank) run concurrently instead of one
+        # or two at a time -- every rank's PCIe link stays busy while NCCL
+        # broadcasts and the kernels consume the batches in order
+        self.nslots = max(2, int(slots) if slots else self.world + 1)
         self.raw = [torch.empty((self.batch, self.H, self.W), dtype=torch.float32,
-                                device=self.device) for _ in range(2)]
-        self.packed = [torch.empty(self.batch * nb, dtype=torch.uint8, device=self.device)
-                       for _ in range(2)]
+                                device=self.device) for _ in range(self.nslots)]
+        # one packed buffer: pack and back-projection of a batch are ordered on
+        # the compute stream
+        self.packed = torch.empty(self.batch * nb, dtype=torch.uint8, device=self.device)
         self.vol = torch.zeros(((self.z1 - self.z0), L, L), dtype=torch.float32,
                                device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -190,7 +196,9 @@ class DistributedReconstructor:
         buf = self.raw[slot][:n]
         if self.cuda:
             cur = torch.cuda.current_stream(self.device)
-            self.copy_stream.wait_stream(cur)  # raw[slot] free (pack of batch b-2 done)
+            # raw[slot] free: its last reader (the pack of batch b - nslots) is
+            # already enqueued on the compute stream
+            self.copy_stream.wait_stream(cur)
             with torch.cuda.stream(self.copy_stream):
                 if self.rank == root:
                     src = host_imgs[first:first + n]
@@ -225,23 +233,26 @@ class DistributedReconstructor:
             self.vol.zero_()
         self.err.zero_()
         plan = batch_roots(count, self.batch, self.world)
-        pending = self._send(0, host_imgs, *plan[0]) if plan else None
+        depth = self.nslots - 1  # batches sent ahead of the one being computed
+        pending = {}
+        for b in range(min(depth, len(plan))):
+            pending[b] = self._send(b % self.nslots, host_imgs, *plan[b])
         for b, (first, n, root) in enumerate(plan):
-            slot = b & 1
-            nxt = None
-            if b + 1 < len(plan):
-                nxt = self._send(slot ^ 1, host_imgs, *plan[b + 1])
-            if self.cuda and pending is not None:
-                if isinstance(pending, torch.cuda.Event):
-                    torch.cuda.current_stream(self.device).wait_event(pending)
+            slot = b % self.nslots
+            if b + depth < len(plan):
+                pending[b + depth] = self._send((b + depth) % self.nslots, host_imgs,
+                                                *plan[b + depth])
+            done = pending.pop(b)
+            if self.cuda and done is not None:
+                if isinstance(done, torch.cuda.Event):
+                    torch.cuda.current_stream(self.device).wait_event(done)
                 else:
-                    pending.wait()
+                    done.wait()
             if root == self.rank and hooks.check is not None:
                 hooks.check(self.raw[slot][:n], self.err)
-            hooks.pack(self.raw[slot][:n], self.packed[slot], self.err)
-            hooks.backproject(self.vol, self.z0, self.z1, self.packed[slot], n,
+            hooks.pack(self.raw[slot][:n], self.packed, self.err)
+            hooks.backproject(self.vol, self.z0, self.z1, self.packed, n,
                               m[first:first + n], self.err)
-            pending = nxt
         # every rank raises the same error: OR of the flags (bit 1: w == 0,
         # bit 2: non-finite pixel) over the group
         flags = torch.stack([(self.err & 1) != 0, (self.err & 2) != 0]).to(torch.int32)
