@@ -8,10 +8,15 @@
 
 namespace cbb {
 
-// Ring slots per device (raw, packed, pinned host staging). Two suffice: a
-// third did not speed up pageable sources (measured 97.6 vs 96-97 ms on
-// config 2), whose host copies contend with the H2D DMA for host memory.
-constexpr int kSlots = 2;
+// Raw-projection ring per device: G + 1 slots for G devices (at most
+// kMaxSlots), so with rotating upload roots the next G uploads -- one per
+// device -- are in flight together; with two slots they would serialise
+// (2.8 ms per 153 MB batch against ~0.7 ms of kernels per batch at G = 8).
+// Pinned host staging for pageable sources is a separate ring of two (a
+// third did not help: those host copies contend with the DMA for host
+// memory, measured on config 2).
+constexpr int kMaxSlots = 17;
+constexpr int kStageSlots = 2;
 
 // ---------------------------------------------------------------------------
 // Per-device worker: slab volume, raw/packed double buffers, streams, events.
@@ -21,11 +26,11 @@ struct Worker {
     int device = 0;
     int z_begin = 0, z_end = 0;
     float* d_vol = nullptr;
-    float* d_raw[kSlots] = {};
-    void* d_packed[kSlots] = {};
+    float* d_raw[kMaxSlots] = {};
+    void* d_packed = nullptr;          // one batch: pack and kernels share the compute stream
     int* d_err = nullptr;
     cudaStream_t copy = nullptr, compute = nullptr;
-    cudaEvent_t h2d_done[kSlots] = {}, raw_free[kSlots] = {};
+    cudaEvent_t h2d_done[kMaxSlots] = {}, raw_free[kMaxSlots] = {};
     cudaEvent_t k_beg = nullptr, k_end = nullptr, c_beg = nullptr, c_end = nullptr;
     double kernel_s = 0.0, h2d_s = 0.0, d2h_s = 0.0;
     uint64_t guarded = 0;
@@ -41,7 +46,8 @@ struct Worker {
     // detector rows this worker holds / packs (RowBand::full unless set_bands)
     RowBand band;
     size_t pk_bytes = 0;               // packed bytes per projection (band rows)
-    cudaEvent_t src_ready[kSlots] = {}; // as root: raw slot filtered, peers may copy
+    cudaEvent_t src_ready[kMaxSlots] = {}; // as root: raw slot filtered, peers may copy
+    cudaEvent_t stage_read[kStageSlots] = {}; // as root: H2D from host staging slot done
     cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
     unsigned long long* d_counters = nullptr; // kCounterSlots culled-update counters
     bool count_culled = false;
@@ -54,13 +60,19 @@ struct Worker {
         cudaStreamSynchronize(compute);
         auto& pool = DevicePool::get();
         pool.release(device, d_vol);
-        for (int i = 0; i < kSlots; ++i) {
+        for (int i = 0; i < kMaxSlots; ++i) {
             pool.release(device, d_raw[i]);
-            pool.release(device, d_packed[i]);
-            cudaEventDestroy(h2d_done[i]);
-            cudaEventDestroy(raw_free[i]);
-            cudaEventDestroy(src_ready[i]);
+            if (h2d_done[i])
+                cudaEventDestroy(h2d_done[i]);
+            if (raw_free[i])
+                cudaEventDestroy(raw_free[i]);
+            if (src_ready[i])
+                cudaEventDestroy(src_ready[i]);
         }
+        pool.release(device, d_packed);
+        for (auto e : stage_read)
+            if (e)
+                cudaEventDestroy(e);
         for (auto e : xfer_ev)
             cudaEventDestroy(e);
         pool.release(device, d_err);
@@ -144,10 +156,13 @@ struct Pipeline {
     int W = 0, H = 0;
     cbb_options opt{};
     std::vector<std::unique_ptr<Worker>> workers;
-    float* h_stage[kSlots] = {};            // pinned staging (batch x H x W)
+    float* h_stage[kStageSlots] = {};       // pinned staging (batch x H x W)
+    int stage_owner[kStageSlots] = {-1, -1}; // worker whose H2D last read the staging slot
     ChunkedXfer xfer;                       // volume up/download for pageable buffers
     int stage_fill = 0;                     // projections staged in the current slot
-    int slot = 0;                           // current staging / ring slot
+    int sslot = 0;                          // current host staging slot
+    int slot = 0;                           // current device ring slot
+    int nslots = 2;                         // device ring slots in use
     std::vector<double> stage_mats;         // matrices of the staged batch
     uint64_t submitted = 0;
     uint64_t nbatch = 0;   // batches issued (root = nbatch mod workers)
@@ -296,14 +311,17 @@ struct Pipeline {
             CK(cudaSetDevice(w->device));
             CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
             CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));
-            for (int s = 0; s < kSlots; ++s) {
+            nslots = std::min(kMaxSlots, std::max(2, ng + 1));
+            for (int s = 0; s < nslots; ++s) {
                 CK(cudaEventCreateWithFlags(&w->h2d_done[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->raw_free[s], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&w->src_ready[s], cudaEventDisableTiming));
                 w->d_raw[s] = static_cast<float*>(
                     DevicePool::get().alloc(w->device, raw_bytes_per_proj * opt.batch));
-                w->d_packed[s] = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
             }
+            w->d_packed = DevicePool::get().alloc(w->device, packed_bytes_per_proj * opt.batch);
+            for (auto& e : w->stage_read)
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             for (auto& e : w->xfer_ev)
                 CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             w->band = RowBand::full(H);
@@ -362,8 +380,9 @@ struct Pipeline {
 
     // Issues one batch of n projections from host memory src (pinned or not)
     // to every worker. The caller guarantees src stays valid until the
-    // corresponding h2d_done events complete (wait_slot).
-    void issue(const float* src, const double* mats, int n) {
+    // upload completes (wait_stage for the staging ring).
+    // stage >= 0: src is host staging slot `stage` (its reuse waits for this H2D).
+    void issue(const float* src, const double* mats, int n, int stage = -1) {
         NvtxRange range("cbb batch");
         const size_t bytes = raw_bytes_per_proj * n;
         // Batch k is uploaded once, by the root worker k mod G. Each other
@@ -374,7 +393,7 @@ struct Pipeline {
         const int G = (int)workers.size();
         Worker& root = *workers[nbatch % G];
         // raw[slot] of worker w may still be read by its own pack of batch
-        // k-kSlots and, if w was that batch's root, by the other workers'
+        // k-nslots and, if w was that batch's root, by the other workers'
         // band copies (h2d_done) or peer packs (raw_free)
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
@@ -388,6 +407,10 @@ struct Pipeline {
         CK(cudaSetDevice(root.device));
         CK(cudaMemcpyAsync(root.d_raw[slot], src, bytes, cudaMemcpyHostToDevice, root.copy));
         CK(cudaEventRecord(root.h2d_done[slot], root.copy));
+        if (stage >= 0) {
+            CK(cudaEventRecord(root.stage_read[stage], root.copy));
+            stage_owner[stage] = (int)(nbatch % G);
+        }
         CK(cudaStreamWaitEvent(root.compute, root.h2d_done[slot], 0));
         start_timing(root);
         // the root sees the whole batch: it checks the pixels its band skips
@@ -427,7 +450,7 @@ struct Pipeline {
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             void* packed = resident ? static_cast<char*>(w->d_packed_all) + w->pk_bytes * submitted
-                                    : w->d_packed[slot];
+                                    : w->d_packed;
             if (w.get() == &root)
                 launch_pack_band(w->d_raw[slot], 0, H, (long long)W * H, W, H, n, packed, w->band,
                                  w->compute, w->d_err);
@@ -449,7 +472,7 @@ struct Pipeline {
         if (resident)
             std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
         submitted += n;
-        slot = (slot + 1) % kSlots;
+        slot = (slot + 1) % nslots;
     }
 
     void start_timing(Worker& w) {
@@ -509,17 +532,18 @@ struct Pipeline {
         return true;
     }
 
-    // Blocks until no device still reads the staging slot s.
-    void wait_slot(int s) {
-        for (auto& w : workers) {
-            CK(cudaSetDevice(w->device));
-            CK(cudaEventSynchronize(w->h2d_done[s]));
-        }
+    // Blocks until no upload still reads the host staging slot s.
+    void wait_stage(int s) {
+        if (stage_owner[s] < 0)
+            return;
+        auto& w = *workers[stage_owner[s]];
+        CK(cudaSetDevice(w.device));
+        CK(cudaEventSynchronize(w.stage_read[s]));
     }
 
     // Pinned staging for pageable sources, allocated on first use only.
     void ensure_staging() {
-        for (int s = 0; s < kSlots; ++s)
+        for (int s = 0; s < kStageSlots; ++s)
             if (!h_stage[s])
                 h_stage[s] = HostPool::get().alloc(raw_bytes_per_proj * opt.batch);
     }
@@ -527,8 +551,8 @@ struct Pipeline {
     void stage_one(const float* img, const double* m) {
         ensure_staging();
         if (stage_fill == 0)
-            wait_slot(slot);
-        std::memcpy(h_stage[slot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
+            wait_stage(sslot);
+        std::memcpy(h_stage[sslot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
         std::memcpy(stage_mats.data() + 12 * (size_t)stage_fill, m, 12 * sizeof(double));
         if (++stage_fill == opt.batch)
             flush();
@@ -537,7 +561,8 @@ struct Pipeline {
     void flush() {
         if (stage_fill == 0)
             return;
-        issue(h_stage[slot], stage_mats.data(), stage_fill);
+        issue(h_stage[sslot], stage_mats.data(), stage_fill, sslot);
+        sslot = (sslot + 1) % kStageSlots;
         stage_fill = 0;
     }
 
@@ -552,7 +577,7 @@ struct Pipeline {
 
     // Whole-stack submission straight from the caller's buffer: pinned
     // buffers are copied asynchronously in place, pageable ones are staged
-    // through the pinned staging ring (kSlots buffers).
+    // through the pinned staging ring (kStageSlots buffers).
     // First submission of a stack whose matrices are all known: row bands,
     // resident mode, tail estimate.
     void begin_stack(const double* mats, int count) {
@@ -585,9 +610,10 @@ struct Pipeline {
                 issue(src, mats + 12 * (size_t)first, n);
             } else {
                 ensure_staging();
-                wait_slot(slot);
-                parallel_memcpy(h_stage[slot], src, raw_bytes_per_proj * n);
-                issue(h_stage[slot], mats + 12 * (size_t)first, n);
+                wait_stage(sslot);
+                parallel_memcpy(h_stage[sslot], src, raw_bytes_per_proj * n);
+                issue(h_stage[sslot], mats + 12 * (size_t)first, n, sslot);
+                sslot = (sslot + 1) % kStageSlots;
             }
         }
     }
@@ -602,8 +628,8 @@ struct Pipeline {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         for (int first = 0, n = 0; first < count; first += n) {
             n = batch_at(first, count);
-            wait_slot(slot);
-            float* dst = h_stage[slot];
+            wait_stage(sslot);
+            float* dst = h_stage[sslot];
             const int nt = (int)std::min<unsigned>(std::min(8u, hw), (unsigned)n);
             std::vector<std::thread> pool;
             for (int t = 0; t < nt; ++t)
@@ -613,7 +639,8 @@ struct Pipeline {
                 });
             for (auto& th : pool)
                 th.join();
-            issue(dst, mats + 12 * (size_t)first, n);
+            issue(dst, mats + 12 * (size_t)first, n, sslot);
+            sslot = (sslot + 1) % kStageSlots;
         }
     }
 
@@ -659,10 +686,10 @@ struct Pipeline {
         for (int first = 0, n = 0; first < count; first += n) {
             n = batch_at(first, count);
             auto t0 = now();
-            wait_slot(slot);
+            wait_stage(sslot);
             t_wait += ms_since(t0);
             t0 = now();
-            float* dst = h_stage[slot];
+            float* dst = h_stage[sslot];
             std::vector<std::thread> pool;
             std::vector<int> bad(nt, 0);
             for (int t = 0; t < nt; ++t)
@@ -687,7 +714,8 @@ struct Pipeline {
             validate_matrices(mats.data(), n);
             t_read += ms_since(t0);
             t0 = now();
-            issue(dst, mats.data(), n);
+            issue(dst, mats.data(), n, sslot);
+            sslot = (sslot + 1) % kStageSlots;
             t_issue += ms_since(t0);
         }
         if (std::getenv("CBB_TRACE"))
