@@ -198,7 +198,7 @@ struct ChunkedXfer {
             if (!b)
                 b = HostPool::get().alloc(kChunk);
     }
-    // returns after the last chunk left the pageable source
+    // returns once every chunk has reached the device (pageable src)
     void upload(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
         if (bytes == 0)
             return;
@@ -216,6 +216,10 @@ struct ChunkedXfer {
                                cudaMemcpyHostToDevice, st));
             CK(cudaEventRecord(ev[k], st));
         }
+        // the staging chunks are shared by every worker of the pipeline (the
+        // events are not): drain them before the next upload may refill them
+        CK(cudaEventSynchronize(ev[0]));
+        CK(cudaEventSynchronize(ev[1]));
     }
     // pageable dst: blocks until all bytes arrived; pinned dst: asynchronous
     void download(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {
