@@ -4,7 +4,7 @@ pitch, angular range, volume size and voxel size, volume offset from the
 isocentre so the detector is over- or under-filled), random batch sizes,
 1-4 slab workers sharing the GPU (rotating upload roots, row bands, peer band
 copies), resident tail on or off, random initial volumes with -0.0 voxels,
-contiguous / per-image / pageable / file inputs. A few cases use random
+contiguous / per-image / pageable / file / session inputs. A few cases use random
 matrices (w changes sign -> guarded kernel, possibly w == 0 -> GeometryError
 with the volume untouched)."""
 import math
@@ -60,7 +60,7 @@ def test_fuzz_pipeline_vs_oracle(cuda, oracle, monkeypatch, tmp_path, seed):
     status = oracle.reconstruct(ref, g, imgs, mats)
     if r.random() < 0.5:
         monkeypatch.setenv("CBB_NO_RESIDENT", "1")
-    how = ["contiguous", "images", "pageable", "file"][seed % 4]
+    how = ["contiguous", "images", "pageable", "file", "session"][seed % 5]
     v = vol0.copy()
 
     def run():
@@ -72,6 +72,13 @@ def test_fuzz_pipeline_vs_oracle(cuda, oracle, monkeypatch, tmp_path, seed):
                                           pkg.Options(**opts))
         if how == "pageable":
             return pkg.reconstruct_arrays(v, g, np.array(imgs), mats, pkg.Options(**opts))
+        if how == "session":  # per-projection calls, flushed in batches
+            with pkg.Session(g, imgs.shape[2], imgs.shape[1], v, pkg.Options(**opts)) as sess:
+                for i in range(len(mats)):
+                    sess.backproject(imgs[i], mats[i])
+                out, st = sess.finish()
+            v[...] = out
+            return st
         p = str(tmp_path / f"s{seed}.cbps")
         pkg.write_stack(p, pkg.ProjectionStack(g, mats, imgs))
         out, st = pkg.reconstruct_file(p, pkg.Options(**opts), initial=pkg.Volume(g, v))
