@@ -689,3 +689,24 @@ def test_resume_from_partial_volume_is_bitwise(cuda):
         resumed = pkg.read_volume(path)
     pkg.reconstruct(resumed, pkg.ProjectionStack(g, mats[k:], imgs[k:]))
     assert bits_equal(resumed.voxels, expected)
+
+
+def test_plain_c_example_runs_on_the_gpu(cuda, tmp_path):
+    """examples/reconstruct_c.c end to end: plain C, cbb_reconstruct on the GPU."""
+    import os
+    import shutil
+    import subprocess
+
+    from conftest import ROOT
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc on this box")
+    exe = str(tmp_path / "reconstruct_c")
+    lib = os.path.join(ROOT, "paper_1401_3615_b200")
+    subprocess.run(["gcc", "-std=c99", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "reconstruct_c.c"), "-L" + lib,
+                    "-lconebeam_b200", "-Wl,-rpath," + lib, "-lm", "-o", exe],
+                   check=True, capture_output=True, timeout=120)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "voxel updates" in out.stdout

@@ -265,3 +265,23 @@ def test_row_bands_cover_every_tap():
     bad[5, 11] = -5.0  # w(0) < 0 for projection 5
     full = pkg.row_band_for_slab(g, W, H, 0, 8, bad)
     assert (full.raw_row0, full.raw_rows, full.cell_row0, full.cell_rows) == (0, H, 0, qr)
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """include/conebeam_b200.h is plain C99: examples/reconstruct_c.c compiles
+    with -Wall -Wextra -Werror against it, links libconebeam_b200.so and runs
+    (ABI part only: no GPU here)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    exe = str(tmp_path / "reconstruct_c")
+    lib = os.path.join(ROOT, "paper_1401_3615_b200")
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror",
+           "-I" + os.path.join(ROOT, "include"), os.path.join(ROOT, "examples", "reconstruct_c.c"),
+           "-L" + lib, "-lconebeam_b200", "-Wl,-rpath," + lib, "-lm", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, timeout=120)
+    out = subprocess.run([exe, "--abi-only"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "geometry error" in out.stdout
