@@ -519,15 +519,20 @@ def secondary_entries(c):
     sec = [dict(workload=cfg.name, mode=other,
                 **measure(g, pkg.MODE_FAST if other == "fast" else pkg.MODE_EXACT,
                           args.steps, (z0, z1)))]
-    if args.config != 3 and cfg.width == synth.CONFIGS[3].width:
-        g3 = synth.CONFIGS[3].geometry
+    # the other volumes of the same scan (configs 0-3 share it): 1024^3
+    # (config 3, the metric's second size) and 256^3 (config 1, BASELINE's
+    # single-GPU case)
+    for other in (3, 1):
+        if args.config == other or cfg.width != synth.CONFIGS[other].width:
+            continue
+        go = synth.CONFIGS[other].geometry
         if world > 1:
             from paper_1401_3615_b200.distributed import balanced_slabs, plane_work
-            sl3 = balanced_slabs(plane_work(g3, mats, W, H), world)[rank]
+            slo = balanced_slabs(plane_work(go, mats, W, H), world)[rank]
         else:
-            sl3 = (0, g3.edge_voxels)
-        sec.append(dict(workload=synth.CONFIGS[3].name, mode=args.mode,
-                        **measure(g3, mode, 3, sl3)))
+            slo = (0, go.edge_voxels)
+        sec.append(dict(workload=synth.CONFIGS[other].name, mode=args.mode,
+                        **measure(go, mode, 3 if other == 3 else args.steps, slo)))
     # north_star's hardware-texture side number (not parity-exact)
     from paper_1401_3615_b200.backproject import backproject_texture_device
     vt = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
