@@ -285,3 +285,49 @@ def test_c_abi_from_plain_c(tmp_path):
     out = subprocess.run([exe, "--abi-only"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert "geometry error" in out.stdout
+
+
+def test_abi_rejects_invalid_inputs_before_touching_the_gpu():
+    """Argument validation of the C ABI runs before any CUDA call, so it is
+    checked here without a GPU: empty stacks, zero sizes, non-finite
+    matrices, bad options, oversize detectors and null pointers give
+    CBB_ERR_INVALID (1) with the reference's messages; the volume is not
+    touched."""
+    import ctypes as C
+
+    from paper_1401_3615_b200 import _lib
+    from paper_1401_3615_b200.backproject import geometry_c
+
+    L = _lib.lib()
+    g = geometry_c(pkg.VolumeGeometry.centered(8, 1.0))
+    vol = np.full((8, 8, 8), 7.0, np.float32)
+    imgs = np.zeros((2, 4, 5), np.float32)
+    mats = np.zeros((2, 12))
+    mats[:, 0] = mats[:, 4] = mats[:, 11] = 1.0
+
+    def call(geom=g, w=5, h=4, n=2, m=mats, opt=None, v=vol, im=imgs):
+        oc = _lib.OptionsC()
+        L.cbb_options_defaults(C.byref(oc))
+        for k, val in (opt or {}).items():
+            setattr(oc, k, val)
+        st = L.cbb_reconstruct(None if v is None else v.ctypes.data, C.byref(geom),
+                               None if im is None else im.ctypes.data, w, h, n,
+                               m.ctypes.data, C.byref(oc), None)
+        return st, L.cbb_last_error().decode()
+
+    assert call(n=0) == (1, "ProjectionStack: at least one projection required")
+    assert call(w=0)[0] == 1 and "dimensions" in call(w=0)[1]
+    assert call(h=-3)[0] == 1
+    assert call(w=4000, h=4000)[0] == 1 and "too large" in call(w=4000, h=4000)[1]
+    bad = mats.copy()
+    bad[1, 7] = np.nan
+    assert call(m=bad) == (1, "ProjectionMatrix: field 'a[7]' must be finite")
+    assert call(geom=geometry_c(pkg.VolumeGeometry(0, 1.0, 0.0)))[0] == 1
+    assert call(opt={"batch": 0})[0] == 1 and "batch" in call(opt={"batch": 0})[1]
+    assert call(opt={"batch": 33})[0] == 1
+    assert call(opt={"mode": 7})[0] == 1
+    assert call(opt={"slab_begin": 5, "slab_end": 3})[0] == 1
+    assert call(opt={"ramp_filter": 1, "filter_pixel_mm": 0.0})[0] == 1
+    assert call(v=None)[0] == 1 and "null" in call(v=None)[1]
+    assert call(im=None)[0] == 1
+    assert np.all(vol == 7.0)
