@@ -588,10 +588,13 @@ def e2e_entries(c):
         h2d = imgs_h.numel() * 4 + mats.nbytes
         path = "cbb_reconstruct (C ABI), pinned host buffers"
     else:
-        # one process per GPU: batch b uploaded by rank b % N, NCCL broadcast
+        # one process per GPU: batch b uploaded by rank b % N, then NCCL
+        # broadcast (default) or read by every rank's pack over CUDA IPC
+        # (CBB_BENCH_TRANSPORT=ipc, the fused transfer + pack)
         from paper_1401_3615_b200.distributed import DistributedReconstructor, batch_roots
+        transport = os.environ.get("CBB_BENCH_TRANSPORT", "nccl")
         rec = DistributedReconstructor(g, W, H, batch=args.batch, slabs=slabs,
-                                       options=e2e_opt)
+                                       options=e2e_opt, transport=transport)
 
         def e2e_call():
             torch.cuda.synchronize()
@@ -600,7 +603,8 @@ def e2e_entries(c):
             return time.perf_counter() - t0, {"slab_planes": int(slab.shape[0])}
         h2d = sum(n for _, n, r in batch_roots(n_proj, args.batch, world) if r == rank) \
             * H * W * 4 + mats.nbytes
-        path = "DistributedReconstructor: 1/N of batches uploaded per rank + NCCL broadcast"
+        path = ("DistributedReconstructor: 1/N of batches uploaded per rank + " +
+                ("NCCL broadcast" if transport == "nccl" else "pack over CUDA IPC peer memory"))
     e2e_call()  # warm-up
     if dist:
         dist.barrier()

@@ -283,6 +283,21 @@ typedef struct cbb_volume_diff {
 cbb_status cbb_compare_volumes_device(const float* test, const float* ref, int64_t n,
                                       double denom_floor, cbb_volume_diff* out, void* stream);
 
+/* ---- multi-process plumbing (one process per GPU) ------------------------
+ * Device buffers another process can map (CUDA IPC; handle = 64 bytes), and
+ * stream-ordered 32-bit flags (cuStreamWriteValue32 / cuStreamWaitValue32),
+ * so a rank's pack kernel can read the uploading rank's projection slot over
+ * NVLink once that rank has flagged it ready -- the broadcast and the layout
+ * transform become one kernel. cbb_stream_wait_flag blocks the stream until
+ * (int32_t)(*flag - value) >= 0. */
+cbb_status cbb_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle /* 64 bytes */);
+cbb_status cbb_ipc_free(void* dev_ptr);
+cbb_status cbb_ipc_open(const void* handle, void** dev_ptr);
+cbb_status cbb_ipc_close(void* dev_ptr);
+cbb_status cbb_stream_write_flag(void* flag, uint32_t value, void* stream);
+cbb_status cbb_stream_wait_flag(const void* flag, uint32_t value, void* stream);
+cbb_status cbb_memcpy_h2d_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Frees the library's cached device buffers, pinned host staging and texture
  * arrays (kept between calls to avoid allocation costs), like
  * torch.cuda.empty_cache. Call when no other cbb_* call is running. */

@@ -24,7 +24,8 @@ EXPORTS = (
     "cbb_compare_volumes_device", "cbb_stack_file_query", "cbb_reconstruct_file",
     "cbb_backproject_texture_device", "cbb_row_band_for_slab", "cbb_pack_device_band",
     "cbb_backproject_device_band", "cbb_check_finite_device", "cbb_reconstruct_images",
-    "cbb_release_cached_memory",
+    "cbb_release_cached_memory", "cbb_ipc_alloc", "cbb_ipc_free", "cbb_ipc_open",
+    "cbb_ipc_close", "cbb_stream_write_flag", "cbb_stream_wait_flag", "cbb_memcpy_h2d_async",
 )
 
 
@@ -154,6 +155,15 @@ def _declare(L) -> None:
                                               _VP, _VP]
     L.cbb_check_finite_device.restype = C.c_int
     L.cbb_check_finite_device.argtypes = [_VP, C.c_int64, _VP, _VP]
+    for name, args in (("cbb_ipc_alloc", [C.c_int64, C.POINTER(_VP), _VP]),
+                       ("cbb_ipc_free", [_VP]), ("cbb_ipc_open", [_VP, C.POINTER(_VP)]),
+                       ("cbb_ipc_close", [_VP]),
+                       ("cbb_stream_write_flag", [_VP, C.c_uint32, _VP]),
+                       ("cbb_stream_wait_flag", [_VP, C.c_uint32, _VP]),
+                       ("cbb_memcpy_h2d_async", [_VP, _VP, C.c_int64, _VP])):
+        fn = getattr(L, name)
+        fn.restype = C.c_int
+        fn.argtypes = args
     L.cbb_release_cached_memory.restype = C.c_int
     L.cbb_release_cached_memory.argtypes = []
     L.cbb_launch_count.restype = C.c_uint64

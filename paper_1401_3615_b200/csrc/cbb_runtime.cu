@@ -45,6 +45,7 @@
 #include "texture_variant.cuh"
 
 #include "runtime_common.cuh"
+#include "ipc.cuh"
 #include "launch.cuh"
 #include "memory.cuh"
 #include "pipeline.cuh"
@@ -164,6 +165,83 @@ namespace {
 std::mutex g_tex_mu;
 std::map<int, std::tuple<cudaArray_t, int, int, int>> g_tex_arrays; // device -> array, W, H, layers
 } // namespace
+
+// ---- CUDA IPC buffers and stream-ordered flags (multi-process drivers) ----
+
+cbb_status cbb_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle) {
+    return guarded([&] {
+        if (bytes <= 0 || !dev_ptr || !handle)
+            fail(CBB_ERR_INVALID, "cbb_ipc_alloc: bad argument");
+        void* p = nullptr;
+        CK(cudaMalloc(&p, (size_t)bytes));
+        CK(cudaMemset(p, 0, (size_t)bytes));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            CK(e);
+        }
+        std::memcpy(handle, &h, sizeof h);
+        *dev_ptr = p;
+    });
+}
+
+cbb_status cbb_ipc_free(void* dev_ptr) {
+    return guarded([&] {
+        if (dev_ptr) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(dev_ptr));
+        }
+    });
+}
+
+cbb_status cbb_ipc_open(const void* handle, void** dev_ptr) {
+    return guarded([&] {
+        if (!handle || !dev_ptr)
+            fail(CBB_ERR_INVALID, "cbb_ipc_open: null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+cbb_status cbb_ipc_close(void* dev_ptr) {
+    return guarded([&] {
+        if (dev_ptr)
+            CK(cudaIpcCloseMemHandle(dev_ptr));
+    });
+}
+
+cbb_status cbb_stream_write_flag(void* flag, uint32_t value, void* stream) {
+    return guarded([&] {
+        const auto& ops = StreamMemOps::get();
+        if (!ops.write || !flag)
+            fail(CBB_ERR_INTERNAL, "cuStreamWriteValue32 unavailable or null flag");
+        check_cu(ops.write(static_cast<CUstream>(stream), (CUdeviceptr)flag, value,
+                           CU_STREAM_WRITE_VALUE_DEFAULT),
+                 "cuStreamWriteValue32");
+    });
+}
+
+cbb_status cbb_stream_wait_flag(const void* flag, uint32_t value, void* stream) {
+    return guarded([&] {
+        const auto& ops = StreamMemOps::get();
+        if (!ops.wait || !flag)
+            fail(CBB_ERR_INTERNAL, "cuStreamWaitValue32 unavailable or null flag");
+        check_cu(ops.wait(static_cast<CUstream>(stream), (CUdeviceptr)flag, value,
+                          CU_STREAM_WAIT_VALUE_GEQ),
+                 "cuStreamWaitValue32");
+    });
+}
+
+cbb_status cbb_memcpy_h2d_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    return guarded([&] {
+        if (!dst || !src || bytes < 0)
+            fail(CBB_ERR_INVALID, "cbb_memcpy_h2d_async: bad argument");
+        CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice,
+                           static_cast<cudaStream_t>(stream)));
+    });
+}
 
 cbb_status cbb_release_cached_memory(void) {
     return guarded([&] {

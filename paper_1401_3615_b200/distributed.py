@@ -153,7 +153,8 @@ class DistributedReconstructor:
 
     def __init__(self, geometry: VolumeGeometry, width: int, height: int, batch: int = 32,
                  slabs: Optional[Sequence[tuple]] = None, group=None, device=None,
-                 hooks: Optional[Hooks] = None, options=None, slots: Optional[int] = None):
+                 hooks: Optional[Hooks] = None, options=None, slots: Optional[int] = None,
+                 transport: str = "nccl"):
         import torch
         import torch.distributed as dist
 
@@ -188,6 +189,125 @@ class DistributedReconstructor:
                                device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.copy_stream = torch.cuda.Stream(self.device) if self.cuda else None
+        if transport not in ("nccl", "ipc"):
+            raise ValueError("transport must be 'nccl' or 'ipc'")
+        self.transport = transport
+        if transport == "ipc":
+            self._ipc_setup()
+
+    # ---- transport "ipc": fused upload broadcast + pack over peer memory ----
+    #
+    # Each rank owns two raw slots and a flag block (uint32: ready[2], then
+    # consumed[q*2 + j] for every root q and slot j) in CUDA IPC memory that
+    # every other rank maps. Batch b (root q = b mod N, slot j = (b // N) mod 2):
+    # q uploads it into its slot j on its copy stream once every rank flagged
+    # q's upload b - 2N consumed, then flags ready; every rank's compute stream
+    # waits for that flag, runs the band pack straight from q's slot (the
+    # NVLink read and the layout transform are one kernel), flags it consumed
+    # and back-projects. Flags carry a running batch number (never reset).
+    def _ipc_setup(self):
+        import ctypes as C
+
+        from . import _lib
+
+        if not self.cuda:
+            raise ValueError("transport 'ipc' needs CUDA tensors")
+        L = _lib.lib()
+        per = self.batch * self.H * self.W * 4
+        self._nflags = 2 + 2 * self.world
+        local = []
+        for size in (per, per, 4 * self._nflags):
+            ptr, h = C.c_void_p(), (C.c_char * 64)()
+            _lib.check(L.cbb_ipc_alloc(size, C.byref(ptr), h))
+            local.append((ptr.value, bytes(h)))
+        self._ipc_local = [p for p, _ in local]
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, [h for _, h in local], group=self.group)
+        self._ipc_opened = []
+        self._peer = []  # per rank: [raw0, raw1, flags] device pointers
+        for r in range(self.world):
+            if r == self.rank:
+                self._peer.append(list(self._ipc_local))
+                continue
+            ptrs = []
+            for h in handles[r]:
+                ptr = C.c_void_p()
+                _lib.check(L.cbb_ipc_open((C.c_char * 64).from_buffer_copy(h), C.byref(ptr)))
+                ptrs.append(ptr.value)
+                self._ipc_opened.append(ptr.value)
+            self._peer.append(ptrs)
+        self._epoch = 0
+        self.dist.barrier(group=self.group)
+
+    def _raw_view(self, ptr: int, n: int):
+        """A (n, H, W) float32 tensor over device memory at ptr (local or mapped)."""
+        import torch
+
+        class _Arr:
+            __cuda_array_interface__ = {"shape": (n, self.H, self.W), "typestr": "<f4",
+                                        "data": (ptr, False), "version": 3, "strides": None}
+        return torch.as_tensor(_Arr(), device=self.device)
+
+    def _flag(self, rank: int, index: int) -> int:
+        return self._peer[rank][2] + 4 * index
+
+    def _reconstruct_ipc(self, host_imgs, m, hooks):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+
+        L = _lib.lib()
+        plan = batch_roots(m.shape[0], self.batch, self.world)
+        cur = torch.cuda.current_stream(self.device)
+        copy = self.copy_stream
+        copy.wait_stream(cur)
+        base = self._epoch
+        for b, (first, n, q) in enumerate(plan):
+            seq = base + b + 1
+            j = (b // self.world) % 2
+            if self.rank == q:
+                if b >= 2 * self.world:  # q's upload b - 2N consumed by every rank
+                    prev = base + b - 2 * self.world + 1
+                    for r in range(self.world):
+                        _lib.check(L.cbb_stream_wait_flag(self._flag(r, 2 + 2 * q + j), prev,
+                                                          C.c_void_p(copy.cuda_stream)))
+                src = host_imgs[first:first + n]
+                if not isinstance(src, torch.Tensor):
+                    src = torch.from_numpy(np.ascontiguousarray(src))
+                with torch.cuda.stream(copy):
+                    self._raw_view(self._ipc_local[j], n).copy_(src, non_blocking=True)
+                _lib.check(L.cbb_stream_write_flag(self._flag(q, j), seq,
+                                                   C.c_void_p(copy.cuda_stream)))
+            _lib.check(L.cbb_stream_wait_flag(self._flag(q, j), seq, C.c_void_p(cur.cuda_stream)))
+            raw = self._raw_view(self._peer[q][j], n)
+            if q == self.rank and hooks.check is not None:
+                hooks.check(raw, self.err)
+            hooks.pack(raw, self.packed, self.err)
+            _lib.check(L.cbb_stream_write_flag(self._flag(self.rank, 2 + 2 * q + j), seq,
+                                               C.c_void_p(cur.cuda_stream)))
+            hooks.backproject(self.vol, self.z0, self.z1, self.packed, n,
+                              m[first:first + n], self.err)
+        self._epoch += len(plan)
+
+    def close(self):
+        """Releases the IPC mappings and buffers (transport 'ipc')."""
+        if getattr(self, "transport", "nccl") != "ipc" or not hasattr(self, "_ipc_local"):
+            return
+        from . import _lib
+
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier(group=self.group)  # no rank still reads our slots
+        L = _lib.lib()
+        for p in self._ipc_opened:
+            L.cbb_ipc_close(p)
+        for p in self._ipc_local:
+            L.cbb_ipc_free(p)
+        self._ipc_opened, self._ipc_local = [], []
+        self.transport = "closed"
 
     def _send(self, slot: int, host_imgs, first: int, n: int, root: int):
         """Root uploads batch rows [first, first+n) into raw[slot]; broadcast."""
@@ -232,6 +352,11 @@ class DistributedReconstructor:
         else:
             self.vol.zero_()
         self.err.zero_()
+        if self.transport == "ipc":
+            self._reconstruct_ipc(host_imgs, m, hooks)
+            return self._finish()
+        if self.transport != "nccl":
+            raise RuntimeError("DistributedReconstructor is closed")
         plan = batch_roots(count, self.batch, self.world)
         depth = self.nslots - 1  # batches sent ahead of the one being computed
         pending = {}
@@ -253,6 +378,11 @@ class DistributedReconstructor:
             hooks.pack(self.raw[slot][:n], self.packed, self.err)
             hooks.backproject(self.vol, self.z0, self.z1, self.packed, n,
                               m[first:first + n], self.err)
+        return self._finish()
+
+    def _finish(self) -> np.ndarray:
+        import torch
+
         # every rank raises the same error: OR of the flags (bit 1: w == 0,
         # bit 2: non-finite pixel) over the group
         flags = torch.stack([(self.err & 1) != 0, (self.err & 2) != 0]).to(torch.int32)

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, transport="nccl"):
     import torch
     import torch.distributed as dist
 
@@ -38,7 +38,8 @@ def _worker(rank, world, port, q):
         cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=64, num_projections=40)
         g, mats, imgs = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=20)
         slabs = balanced_slabs(plane_work(g, mats, cfg.width, cfg.height), world)
-        rec = DistributedReconstructor(g, cfg.width, cfg.height, batch=6, slabs=slabs)
+        rec = DistributedReconstructor(g, cfg.width, cfg.height, batch=6, slabs=slabs,
+                                       transport=transport)
         slab = rec.reconstruct(imgs.pin_memory(), mats)
         bad = imgs.clone()
         bad[13, 0, 0] = float("nan")  # batch 2 -> uploaded by rank 0
@@ -47,12 +48,19 @@ def _worker(rank, world, port, q):
             err = "none"
         except Exception as e:  # noqa: BLE001
             err = type(e).__name__
-        q.put((rank, np.array(slab), err, slabs))
+        again = rec.reconstruct(imgs.pin_memory(), mats)  # flags keep counting
+        rec.close()
+        q.put((rank, np.array(slab), err, slabs, bool(np.array_equal(again, slab))))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_driver_on_one_gpu(cuda, oracle):
+@pytest.mark.parametrize("transport", ["nccl", "ipc"])
+def test_two_rank_driver_on_one_gpu(cuda, oracle, transport):
+    """transport 'nccl': broadcast of each batch (gloo stands in here);
+    transport 'ipc': every rank's pack reads the uploading rank's slot through
+    CUDA IPC, ordered by stream flags (same device here, NVLink peers on a
+    multi-GPU box)."""
     import torch.multiprocessing as mp
 
     from paper_1401_3615_b200 import synth
@@ -60,7 +68,7 @@ def test_two_rank_driver_on_one_gpu(cuda, oracle):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted((q.get(timeout=180) for _ in range(2)), key=lambda t: t[0])
@@ -76,3 +84,4 @@ def test_two_rank_driver_on_one_gpu(cuda, oracle):
     full = np.concatenate([out[0][1], out[1][1]])
     assert bits_equal(full, ref)
     assert [o[2] for o in out] == ["ValidationError", "ValidationError"]
+    assert all(o[4] for o in out)  # a second call on the same driver, same bits
