@@ -710,3 +710,41 @@ def test_plain_c_example_runs_on_the_gpu(cuda, tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "voxel updates" in out.stdout
+
+
+def test_concurrent_calls_from_host_threads(cuda, oracle):
+    """cbb_reconstruct from four host threads at once (ctypes releases the
+    GIL): each call owns its streams, the buffer caches are locked, so every
+    result is bitwise the sequential one."""
+    import threading
+
+    cases = []
+    for k in range(4):
+        cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=40 + 8 * k, num_projections=20 + 3 * k)
+        g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=10)
+        imgs = imgs_t.numpy()
+        ref = np.zeros((g.edge_voxels,) * 3, np.float32)
+        assert oracle.reconstruct(ref, g, imgs, mats) == 0
+        cases.append((g, mats, imgs, ref))
+    out = [None] * len(cases)
+    errors = []
+
+    def run(i):
+        try:
+            g, mats, imgs, _ = cases[i]
+            for _ in range(3):
+                v = np.zeros((g.edge_voxels,) * 3, np.float32)
+                pkg.reconstruct_arrays(v, g, np.array(imgs), mats,
+                                       pkg.Options(device_ids=[0] * (1 + i % 2), batch=7))
+            out[i] = v
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for (g, mats, imgs, ref), v in zip(cases, out):
+        assert bits_equal(v, ref)
