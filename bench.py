@@ -414,6 +414,11 @@ def run_ours(args):
         c.packed = None
         del packed
         line.update(e2e_entries(c))
+        if line.get("culled_fraction") is not None and line["culled_fraction"] >= 0:
+            # the same fraction counted only over the updates the kernel
+            # computes (the full basis includes the culled, provably-zero ones)
+            line["roofline"]["frac_on_computed_updates"] = round(
+                line["roofline"]["frac"] * (1.0 - line["culled_fraction"]), 4)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_entry(c)
     if rank == 0:
