@@ -93,3 +93,11 @@ def test_fuzz_pipeline_vs_oracle(cuda, oracle, monkeypatch, tmp_path, seed):
         return
     run()
     assert bits_equal(v, ref), (seed, how, opts)
+    if seed % 3 == 0 and seed % 7 != 3:  # fast mode within north_star's tolerance
+        fast = pkg.Volume(g, vol0.copy())
+        pkg.reconstruct(fast, pkg.ProjectionStack(g, mats, imgs),
+                        pkg.Options(**dict(opts, mode=pkg.MODE_FAST)))
+        d = fast.voxels.astype(np.float64) - ref
+        rng = float(ref.max() - ref.min()) or 1.0
+        assert np.linalg.norm(d) <= 1e-5 * max(np.linalg.norm(ref.astype(np.float64)), 1e-30)
+        assert np.abs(d).max() <= 1e-4 * rng
