@@ -103,30 +103,35 @@ void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st)
 }
 
 template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false,
-          bool SOA = false, int TW = 8>
+          bool SOA = false, int TW = 8, int BY = kBlockY>
 void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
-    args.nby = (args.L + kBlockY - 1) / kBlockY;
+    args.nby = (args.L + BY - 1) / BY;
     args.nbz = (nz - args.gap + R - 1) / R;
-    dim3 block(kBlockX * kBlockY);
+    dim3 block(kBlockX * BY);
     dim3 grid(args.nbx, args.nby, args.nbz);
     if (SW) {
         const long long ns = (long long)((args.nbx + kSX - 1) / kSX) *
                              ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
         grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
     }
-    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA, TW><<<grid, block, 0, st>>>(args, mats);
+    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA, TW, BY><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
 
 // Kernel shape variant (tuning experiments; CBB_BP_VARIANT overrides):
-// 0 = R 8 voxels/thread, 3 blocks/SM, voxel-internal pairs (default, measured
-// best on config 2); 1 = R 4, 4 blocks/SM; 2 = R 8, 2 blocks/SM; 3 = R 4 with
-// super-tile order; 4 = the default shape with voxel-pair lanes (SOA); 5 =
-// the default; 6 / 7 / 8 = warp tiles of 16x2 / 4x8 / 32x1 voxels instead of
-// 8x4 (783 / 784 / 774 vs 784 GUp/s exact on config 2).
+// 0 = R 8 voxels/thread, 8x4-voxel warp tiles, 4-warp blocks at 6 blocks/SM,
+// voxel-internal pairs (default, measured best on configs 2 and 3). The rest
+// use 8-warp blocks at 3 blocks/SM: 1 = R 4, 4 blocks/SM; 2 = R 8, 2
+// blocks/SM; 3 = R 4 with super-tile order; 4 = voxel-pair lanes (SOA); 5 =
+// the default tile (the v9 shape); 6 / 7 / 8 = warp tiles of 16x2 / 4x8 /
+// 32x1 voxels instead of 8x4 (783 / 784 / 774 vs 784 GUp/s exact on config 2).
+// Measured and dropped (config 2, exact, vs 790 for variant 5 and 803 for
+// the default): 4-warp blocks at 7 blocks/SM (72 registers) 761, at 8
+// blocks/SM (64 registers, spills) 715; 16x2 tiles in 4-warp blocks 800;
+// 2-warp blocks 770 (16x2 tiles) / 747 (32x1 tiles); 1-warp blocks 682-685.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
@@ -137,19 +142,19 @@ void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st
     if (GUARD) // (culling does not run in the guarded kernel: nothing to count)
         return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
     if (args.counters) // statistics requested: the counting instantiation
-        return launch_bp_r<8, MODE, GUARD, 3, 0, true>(args, mats, nz, st);
+        return launch_bp_r<8, MODE, GUARD, 6, 0, true, false, 8, 4>(args, mats, nz, st);
     switch (bp_variant()) {
     case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
     case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
     case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
     case 4: return launch_bp_r<8, MODE, GUARD, 3, 0, false, true>(args, mats, nz, st);
-    case 5: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false>(args, mats, nz, st);
+    case 5: return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
     case 6: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 16>(args, mats, nz, st);
     case 7: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 4>(args, mats, nz, st);
     case 8: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 32>(args, mats, nz, st);
-    default: // voxel-internal pairs: 784 (exact) / 873 (fast) GUp/s on config 2 vs
-             // 764 / 866 with voxel-pair lanes (variant 4)
-        return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
+    default: // 8x4 warp tiles in 4-warp blocks, 6 blocks/SM: 803 (exact) / 898
+             // (fast) GUp/s on config 2 vs 790 / 879 with 8-warp blocks (variant 5)
+        return launch_bp_r<8, MODE, GUARD, 6, 0, false, false, 8, 4>(args, mats, nz, st);
     }
 }
 
