@@ -133,6 +133,7 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
 // blocks/SM (64 registers, spills) 715; 16x2 tiles in 4-warp blocks 800;
 // 2-warp blocks 770 (16x2 tiles) / 747 (32x1 tiles); 1-warp blocks 682-685;
 // 4-warp blocks at 5 blocks/SM (96 registers) 784; R = 4 in 4-warp blocks 746.
+// Gathers as ld.global.cg: 799 (no change); with L1::no_allocate: 724.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
