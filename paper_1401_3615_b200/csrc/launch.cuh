@@ -103,7 +103,7 @@ void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st)
 }
 
 template <int R, int MODE, bool GUARD, int MINB, int SW = 0, bool CNT = false,
-          bool SOA = false, int TW = 8, int BY = kBlockY>
+          bool SOA = false, int TW = 8, int BY = kBlockY, bool BIGI = false>
 void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
     BpArgs args = a;
     args.nbx = (args.L + kBlockX - 1) / kBlockX;
@@ -116,7 +116,7 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
                              ((args.nby + kSY - 1) / kSY) * ((args.nbz + kSZ - 1) / kSZ);
         grid = dim3((unsigned)(ns * kSX * kSY * kSZ), 1, 1);
     }
-    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA, TW, BY><<<grid, block, 0, st>>>(args, mats);
+    bp_kernel<R, MODE, GUARD, MINB, SW, CNT, SOA, TW, BY, BIGI><<<grid, block, 0, st>>>(args, mats);
     CK(cudaGetLastError());
     ++g_launches;
 }
@@ -139,24 +139,37 @@ int bp_variant() {
     return e ? std::atoi(e) : 0;
 }
 
+// bigi: the packed grid has >= 2^23 cells (detectors beyond ~2800 x 2800):
+// integer cell indices, default shape only.
 template <int MODE, bool GUARD>
-void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st) {
-    if (GUARD) // (culling does not run in the guarded kernel: nothing to count)
-        return launch_bp_r<kR, MODE, GUARD, 2>(args, mats, nz, st);
-    if (args.counters) // statistics requested: the counting instantiation
-        return launch_bp_r<8, MODE, GUARD, 6, 0, true, false, 8, 4>(args, mats, nz, st);
-    switch (bp_variant()) {
-    case 1: return launch_bp_r<4, MODE, GUARD, 4>(args, mats, nz, st);
-    case 2: return launch_bp_r<8, MODE, GUARD, 2>(args, mats, nz, st);
-    case 3: return launch_bp_r<4, MODE, GUARD, 4, 1>(args, mats, nz, st);
-    case 4: return launch_bp_r<8, MODE, GUARD, 3, 0, false, true>(args, mats, nz, st);
-    case 5: return launch_bp_r<8, MODE, GUARD, 3>(args, mats, nz, st);
-    case 6: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 16>(args, mats, nz, st);
-    case 7: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 4>(args, mats, nz, st);
-    case 8: return launch_bp_r<8, MODE, GUARD, 3, 0, false, false, 32>(args, mats, nz, st);
-    default: // 8x4 warp tiles in 4-warp blocks, 6 blocks/SM: 803 (exact) / 898
-             // (fast) GUp/s on config 2 vs 790 / 879 with 8-warp blocks (variant 5)
-        return launch_bp_r<8, MODE, GUARD, 6, 0, false, false, 8, 4>(args, mats, nz, st);
+void launch_bp_t(const BpArgs& args, const BpMats& mats, int nz, cudaStream_t st, bool bigi) {
+    if constexpr (GUARD) { // (culling does not run here: nothing to count)
+        if (bigi)
+            return launch_bp_r<kR, MODE, true, 2, 0, false, false, 8, kBlockY, true>(args, mats,
+                                                                                   nz, st);
+        return launch_bp_r<kR, MODE, true, 2>(args, mats, nz, st);
+    } else {
+        if (bigi) {
+            if (args.counters)
+                return launch_bp_r<8, MODE, false, 6, 0, true, false, 8, 4, true>(args, mats, nz,
+                                                                                 st);
+            return launch_bp_r<8, MODE, false, 6, 0, false, false, 8, 4, true>(args, mats, nz, st);
+        }
+        if (args.counters) // statistics requested: the counting instantiation
+            return launch_bp_r<8, MODE, false, 6, 0, true, false, 8, 4>(args, mats, nz, st);
+        switch (bp_variant()) {
+        case 1: return launch_bp_r<4, MODE, false, 4>(args, mats, nz, st);
+        case 2: return launch_bp_r<8, MODE, false, 2>(args, mats, nz, st);
+        case 3: return launch_bp_r<4, MODE, false, 4, 1>(args, mats, nz, st);
+        case 4: return launch_bp_r<8, MODE, false, 3, 0, false, true>(args, mats, nz, st);
+        case 5: return launch_bp_r<8, MODE, false, 3>(args, mats, nz, st);
+        case 6: return launch_bp_r<8, MODE, false, 3, 0, false, false, 16>(args, mats, nz, st);
+        case 7: return launch_bp_r<8, MODE, false, 3, 0, false, false, 4>(args, mats, nz, st);
+        case 8: return launch_bp_r<8, MODE, false, 3, 0, false, false, 32>(args, mats, nz, st);
+        default: // 8x4 warp tiles in 4-warp blocks, 6 blocks/SM: 803 (exact) / 898
+                 // (fast) GUp/s on config 2 vs 790 / 879 with 8-warp blocks (variant 5)
+            return launch_bp_r<8, MODE, false, 6, 0, false, false, 8, 4>(args, mats, nz, st);
+        }
     }
 }
 
@@ -187,6 +200,9 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     args.Hf = (float)H;
     args.qpitchf = (float)qp;
     args.cell_bias = (float)(kPad * qp + kPad) + 8388608.0f;
+    args.qpitch = qp;
+    args.cell_base = kPad * qp + kPad + kMagic;
+    const bool bigi = (double)qp * quad_rows(H) >= kFloatCells;
     args.err = err;
     args.counters = counters;
     args.neg_zero2 = 0x8000000080000000ull;
@@ -221,14 +237,14 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
                       (long long)kMagic * 16 - band_shift;
         if (opt.mode == CBB_MODE_EXACT) {
             if (safe)
-                launch_bp_t<0, false>(args, m, nz, st);
+                launch_bp_t<0, false>(args, m, nz, st, bigi);
             else
-                launch_bp_t<0, true>(args, m, nz, st);
+                launch_bp_t<0, true>(args, m, nz, st, bigi);
         } else {
             if (safe)
-                launch_bp_t<1, false>(args, m, nz, st);
+                launch_bp_t<1, false>(args, m, nz, st, bigi);
             else
-                launch_bp_t<1, true>(args, m, nz, st);
+                launch_bp_t<1, true>(args, m, nz, st, bigi);
         }
         guarded_launches += safe ? 0 : 1;
     }

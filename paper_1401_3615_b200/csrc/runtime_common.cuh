@@ -88,9 +88,10 @@ void validate_geometry(const cbb_volume_geometry* g) {
 void validate_detector(int32_t w, int32_t h) {
     if (w < 1 || h < 1)
         fail(CBB_ERR_INVALID, "ProjectionImage: dimensions must be >= 1");
-    // packed cell indices are formed exactly in float: must stay below 2^23
+    // packed cell indices (kMagic-biased int32, see cell_index) must stay
+    // below 2^31: detectors up to ~29800 x 29800
     const double cells = (double)quad_pitch_cells(w) * quad_rows(h);
-    if (cells >= 8388608.0 - 16)
+    if (cells >= kMaxCells)
         fail(CBB_ERR_INVALID, "detector %dx%d too large for the packed layout", w, h);
 }
 

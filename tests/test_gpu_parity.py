@@ -475,6 +475,31 @@ def test_config0_geometry_bitwise(cuda, oracle):
     assert rel_l2(fv, ref) <= REL_L2_TOL and max_abs_over_range(fv, ref) <= MAX_ABS_TOL
 
 
+def test_large_detector_integer_cell_indices(cuda, oracle, monkeypatch):
+    """A 3600 x 2800 detector (packed grid 3696 x 2896 = 10.7M cells, past the
+    2^23 of the float cell index): the integer-index kernels -- fast path,
+    counting instantiation, guarded kernel -- bitwise against the oracle."""
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=48, num_projections=8, width=3600,
+                       height=2800)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=4)
+    imgs = imgs_t.numpy()
+    assert pkg.packed_layout(3600, 2800)[0] * pkg.packed_layout(3600, 2800)[1] > 2 ** 23
+    ref = np.zeros((48,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs, mats) == 0
+    assert np.count_nonzero(ref) > 0.5 * ref.size
+    v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref))
+    assert st["guarded_batches"] == 0
+    assert bits_equal(v, ref)
+    v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), count_culled=1)
+    assert bits_equal(v, ref)
+    fv, _ = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), mode=pkg.MODE_FAST)
+    assert rel_l2(fv, ref) <= REL_L2_TOL and max_abs_over_range(fv, ref) <= MAX_ABS_TOL
+    monkeypatch.setenv("CBB_FORCE_GUARDED", "1")
+    v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref))
+    assert st["guarded_batches"] > 0
+    assert bits_equal(v, ref)
+
+
 @pytest.mark.slow
 def test_config2_full_size_planes_bitwise(cuda, oracle):
     """Full BASELINE config 2 (512^3, 496 x 1248x960): whole volume on the

@@ -318,7 +318,7 @@ def test_abi_rejects_invalid_inputs_before_touching_the_gpu():
     assert call(n=0) == (1, "ProjectionStack: at least one projection required")
     assert call(w=0)[0] == 1 and "dimensions" in call(w=0)[1]
     assert call(h=-3)[0] == 1
-    assert call(w=4000, h=4000)[0] == 1 and "too large" in call(w=4000, h=4000)[1]
+    assert call(w=40000, h=40000)[0] == 1 and "too large" in call(w=40000, h=40000)[1]
     bad = mats.copy()
     bad[1, 7] = np.nan
     assert call(m=bad) == (1, "ProjectionMatrix: field 'a[7]' must be finite")
