@@ -183,6 +183,11 @@ def test_status_names_and_layout_without_gpu():
     assert qp % 8 == 0 and qp >= 1248 + 96 and qr == 960 + 96 and nb == qp * qr * 16 + 16
     with pytest.raises(pkg.ValidationError):
         pkg.packed_layout(0, 10)
+    # past 2^23 cells the kernels form integer cell indices; the layout stays
+    qp, qr, nb = pkg.packed_layout(3600, 2800)
+    assert qp * qr > 2 ** 23 and nb == qp * qr * 16 + 16
+    with pytest.raises(pkg.ValidationError):  # kMagic + cell index must fit int32
+        pkg.packed_layout(40000, 40000)
 
 
 def test_struct_layouts_match_header():
