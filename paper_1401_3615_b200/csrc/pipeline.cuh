@@ -570,10 +570,24 @@ struct Pipeline {
     // 16, ... up to opt.batch, so the first back-projection starts after a
     // small upload instead of a full batch (pipeline fill). Batch boundaries
     // do not change any result: each voxel still accumulates the projections
-    // one by one in stack order.
+    // one by one in stack order. The ramp's three extra launches each re-read
+    // and re-write the slab (~2 x slab bytes at ~6.5 TB/s) while it saves the
+    // upload of (batch - 4) projections (~55 GB/s): no ramp when that costs
+    // more (config 3's 4.3 GB slab: 631 vs 633 ms end to end; config 2:
+    // 86.0 with the ramp vs 87.9 ms without).
     int batch_at(int first, int count) const {
-        return std::min({opt.batch, std::max(4, first), count - first});
+        if (ramp_ < 0) {
+            size_t slab = 0;
+            for (auto& w : workers)
+                slab = std::max(slab, (size_t)(w->z_end - w->z_begin) * g.edge_voxels *
+                                          g.edge_voxels * sizeof(float));
+            const double cost = 3.0 * 2.0 * (double)slab / 6.5e12;
+            const double gain = (double)std::max(0, opt.batch - 4) * W * H * 4.0 / 55e9;
+            ramp_ = gain > cost ? 4 : opt.batch;
+        }
+        return std::min({opt.batch, std::max(ramp_, first), count - first});
     }
+    mutable int ramp_ = -1; // smallest first batch, chosen on first use
 
     // Whole-stack submission straight from the caller's buffer: pinned
     // buffers are copied asynchronously in place, pageable ones are staged
