@@ -42,7 +42,7 @@ struct Worker {
     // head is copied back
     void* d_packed_all = nullptr;
     int tail_lo = 0, tail_hi = 0;
-    cudaEvent_t head_done = nullptr, tail_done = nullptr;
+    cudaEvent_t head_done = nullptr, tail_done = nullptr, tail_mid_done = nullptr;
     // detector rows this worker holds / packs (RowBand::full unless set_bands)
     RowBand band;
     size_t pk_bytes = 0;               // packed bytes per projection (band rows)
@@ -82,6 +82,8 @@ struct Worker {
             cudaEventDestroy(head_done);
         if (tail_done)
             cudaEventDestroy(tail_done);
+        if (tail_mid_done)
+            cudaEventDestroy(tail_mid_done);
         cudaEventDestroy(k_beg);
         cudaEventDestroy(k_end);
         cudaEventDestroy(c_beg);
@@ -213,6 +215,7 @@ struct Pipeline {
             if (!w->head_done) {
                 CK(cudaEventCreate(&w->head_done));
                 CK(cudaEventCreateWithFlags(&w->tail_done, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&w->tail_mid_done, cudaEventDisableTiming));
             }
         }
         resident = true;
@@ -819,16 +822,35 @@ struct Pipeline {
                 xfer.download(vol_out + plane * z0, w.d_vol + plane * (z0 - w.z_begin),
                               plane * (z1 - z0) * sizeof(float), w.copy, w.xfer_ev);
         };
+        // the tail in two parts: its last 8 planes go last, so that only
+        // their download (not the whole tail's) follows the final kernel --
+        // when that saves more (tail download at ~50 GB/s) than the second
+        // part's extra launches cost (~30 us each): config 3 625 vs 631 ms
+        // end to end; configs 0 and 1 lose ~0.7 ms if split.
+        const int nlaunch = (resident_count + opt.batch - 1) / opt.batch;
+        auto tail_mid = [&](const Worker& w) {
+            const double saved_ms = (double)(w.tail_hi - w.tail_lo - 8) * plane * 4.0 / 50e6;
+            return w.tail_hi - w.tail_lo >= 16 && saved_ms > 0.03 * nlaunch ? w.tail_hi - 8
+                                                                            : w.tail_hi;
+        };
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
             if (trace && w == workers.front()) {
                 CK(cudaEventCreate(&t_tail));
                 CK(cudaEventRecord(t_tail, w->compute));
             }
-            w->guarded += launch_backproject(
-                w->d_vol + plane * (w->tail_lo - w->z_begin), g, w->tail_lo, w->tail_hi,
-                w->d_packed_all, W, H, resident_count, all_mats.data(), opt, w->d_err,
-                w->compute, 0, 0, &w->band, w->count_culled ? w->d_counters : nullptr);
+            const int mid = tail_mid(*w);
+            for (const auto& part : {std::make_pair(w->tail_lo, mid),
+                                     std::make_pair(mid, w->tail_hi)}) {
+                if (part.second > part.first)
+                    w->guarded += launch_backproject(
+                        w->d_vol + plane * (part.first - w->z_begin), g, part.first,
+                        part.second, w->d_packed_all, W, H, resident_count, all_mats.data(), opt,
+                        w->d_err, w->compute, 0, 0, &w->band,
+                        w->count_culled ? w->d_counters : nullptr);
+                if (part.second == mid)
+                    CK(cudaEventRecord(w->tail_mid_done, w->compute));
+            }
             CK(cudaEventRecord(w->tail_done, w->compute));
             if (w->started) { // kernel time ends with the tail, not the downloads
                 CK(cudaEventRecord(w->k_end, w->compute));
@@ -849,8 +871,13 @@ struct Pipeline {
             }
             for (auto& w : workers) {
                 CK(cudaSetDevice(w->device));
+                CK(cudaStreamWaitEvent(w->copy, w->tail_mid_done, 0));
+                d2h(*w, w->tail_lo, tail_mid(*w));
+            }
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
                 CK(cudaStreamWaitEvent(w->copy, w->tail_done, 0));
-                d2h(*w, w->tail_lo, w->tail_hi);
+                d2h(*w, tail_mid(*w), w->tail_hi);
                 CK(cudaEventRecord(w->c_end, w->copy));
             }
         }
