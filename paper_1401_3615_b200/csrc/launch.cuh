@@ -134,6 +134,9 @@ void launch_bp_r(const BpArgs& a, const BpMats& mats, int nz, cudaStream_t st) {
 // 2-warp blocks 770 (16x2 tiles) / 747 (32x1 tiles); 1-warp blocks 682-685;
 // 4-warp blocks at 5 blocks/SM (96 registers) 784; R = 4 in 4-warp blocks 746.
 // Gathers as ld.global.cg: 799 (no change); with L1::no_allocate: 724.
+// z-products wz*(a6, a7), wz*a8 as FMUL2s from per-thread plane coordinates
+// instead of broadcast LDS.64 from the block tables (fewer L1 wavefronts,
+// more FMA-pipe work): 745 vs 806 exact, 825 vs 903 fast; config 3 811 vs 861.
 int bp_variant() {
     const char* e = std::getenv("CBB_BP_VARIANT");
     return e ? std::atoi(e) : 0;
