@@ -433,15 +433,18 @@ def roofline_entry(c, bp_ms, nbatch, clocks):
     FP32 ops / measured launch time vs the FP32 peak, with the gather (L1)
     and HBM rates alongside and the ncu DRAM traffic per launch."""
     args, cfg, L, z0, z1, nb = c.args, c.cfg, c.L, c.z0, c.z1, c.nb
+    # per launch on average: the step's updates over its nbatch launches (the
+    # last launch of a step may hold fewer than args.batch projections)
     bp_launch_ms = statistics.mean(bp_ms) / nbatch
-    updates_per_launch = (z1 - z0) * L * L * args.batch
+    proj_per_launch = c.n / nbatch
+    updates_per_launch = (z1 - z0) * L * L * proj_per_launch
     peaks, peak_src = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = c.torch.cuda.get_device_properties(c.dev).multi_processor_count
     fp32_peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lane-ops/s (Tops) at max clock
     achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
     sm_load = clocks.get("sm_mhz") or sm_max
-    hbm_bytes = 8 * (z1 - z0) * L * L + args.batch * nb  # volume rmw + packed inputs
+    hbm_bytes = 8 * (z1 - z0) * L * L + proj_per_launch * nb  # volume rmw + packed inputs
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
