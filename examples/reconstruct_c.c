@@ -57,6 +57,15 @@ int main(int argc, char** argv) {
         sum += vol[k];
     printf("%.3g voxel updates in %.3f ms, volume sum %.6g\n", (double)st.voxel_updates,
            st.total_seconds * 1e3, sum);
+    /* Volume::validate semantics (proj/src/dataset.cpp:146-151): a non-finite
+     * voxel is rejected with CBB_ERR_INVALID and the volume is not touched */
+    const float keep = vol[1234];
+    vol[4321] = NAN;
+    const cbb_status bad = cbb_reconstruct(vol, &g, imgs, W, H, N, mats, &opt, NULL);
+    printf("nan voxel: status %d \"%s\" (%s)\n", (int)bad, cbb_last_error(),
+           vol[1234] == keep && isnan(vol[4321]) ? "volume unchanged" : "VOLUME CHANGED");
+    if (bad != CBB_ERR_INVALID || vol[1234] != keep)
+        return 1;
     free(mats);
     free(imgs);
     free(vol);

@@ -74,7 +74,8 @@ enum {
 /* Options (the B200 counterpart of cb_opt_options, capi.h:84-91). */
 typedef struct cbb_options {
     int32_t num_gpus;          /* 0 = all visible devices (whole-stack calls) */
-    const int32_t* device_ids; /* nullable: devices 0..num_gpus-1 */
+    const int32_t* device_ids; /* nullable: devices 0..num_gpus-1; else num_gpus ids
+                                  (num_gpus must then be > 0: it is the array length) */
     int32_t batch;             /* projections per kernel launch, 1..32 (default 32) */
     int32_t mode;              /* CBB_MODE_EXACT / CBB_MODE_FAST */
     int32_t cull;              /* skip voxel tiles whose footprint misses the detector */
@@ -120,7 +121,14 @@ cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry,
 
 /* All projections in order: reconstruct_reference / cb_reconstruct_optimized
  * (proj/src/kernel_ref.cpp:32-38, capi.h:104-107). imgs holds count*height*width
- * floats, mats count*12 doubles. Multi-GPU: z-slabs, one host thread per GPU. */
+ * floats, mats count*12 doubles. The input volume is validated like
+ * Volume::validate (proj/src/dataset.cpp:146-151): a non-finite voxel gives
+ * CBB_ERR_INVALID and the volume is left unchanged (skipped when
+ * options->volume_is_zero promises zeros). Multi-GPU: work-balanced z-slabs,
+ * one per device, all driven from the calling thread; each batch is uploaded
+ * once and the other devices read their row bands over peer memory (P2P
+ * loads inside the pack kernel, not an NCCL broadcast -- NCCL is used by the
+ * one-process-per-GPU driver, paper_1401_3615_b200/distributed.py). */
 cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry,
                            const float* imgs, int32_t width, int32_t height,
                            int32_t count, const double* mats,
@@ -159,8 +167,14 @@ cbb_status cbb_stack_file_query(const char* path, cbb_stack_file_info* out);
 
 /* Reconstructs a CBPS file into vol (L^3 floats, accumulated like
  * cbb_reconstruct), streaming the projection records from disk into pinned
- * double buffers overlapped with the device work; memory use is independent
- * of the projection count. Non-finite pixels -> CBB_ERR_INVALID. */
+ * double buffers overlapped with the device work: HOST memory use is
+ * independent of the projection count. DEVICE memory is not: when the whole
+ * packed stack fits in HBM with 2 GB to spare, every packed projection is kept
+ * resident (count x cbb_packed_layout bytes per device, ~61 GB for 1440 x
+ * 1536^2) so the last planes can be finished from HBM while the head of the
+ * volume downloads; the buffer stays in the library's cache until
+ * cbb_release_cached_memory (set CBB_NO_RESIDENT=1 to stream only).
+ * Non-finite pixels or voxels -> CBB_ERR_INVALID. */
 cbb_status cbb_reconstruct_file(float* vol, const char* path, const cbb_options* options,
                                 cbb_run_stats* stats);
 
@@ -168,7 +182,8 @@ cbb_status cbb_reconstruct_file(float* vol, const char* path, const cbb_options*
 
 typedef struct cbb_session_s cbb_session;
 
-/* initial_volume (L^3 floats, nullable = zeros) is copied at creation. */
+/* initial_volume (L^3 floats, nullable = zeros) is copied and validated at
+ * creation (non-finite voxel -> CBB_ERR_INVALID, no session is created). */
 cbb_status cbb_session_create(const cbb_volume_geometry* geometry, int32_t width,
                               int32_t height, const float* initial_volume,
                               const cbb_options* options, cbb_session** out);

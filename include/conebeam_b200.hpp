@@ -57,6 +57,14 @@ inline void reconstruct(conebeam::Volume& vol, const conebeam::ProjectionStack& 
     stack.validate();
     if (vol.geometry != stack.geometry)
         throw conebeam::geometry_error("reconstruct_reference: volume and stack geometries differ");
+    // backproject_reference's checks for every projection (kernel_ref.cpp:6-9),
+    // made once up front: the volume (finite, L^3 voxels -- the library reads
+    // and writes L^3 floats through vol.voxels) and unpadded images. Unlike
+    // the reference, nothing has been accumulated when one of them throws.
+    vol.validate();
+    for (const auto& img : stack.images)
+        if (img.padded())
+            throw conebeam::validation_error("backproject_reference requires an unpadded image");
     const int W = stack.images.front().width, H = stack.images.front().height;
     // the images stay where they are (one buffer each); only the 96-byte
     // matrices are gathered

@@ -70,5 +70,43 @@ int main() {
         threw = true;
     }
     std::printf("w0_geometry_error %d\n", threw ? 1 : 0);
-    return (hr == 0xab67551f9fba3780ull && hg == hr && h1 == hr && threw) ? 0 : 1;
+
+    // backproject_reference's validation (kernel_ref.cpp:6-9) through the
+    // adapter: a non-finite voxel, a short voxel buffer and a padded image each
+    // raise validation_error and leave the volume untouched
+    auto raises_validation = [&](auto&& fn) {
+        try {
+            fn();
+        } catch (const validation_error&) {
+            return true;
+        } catch (...) {
+        }
+        return false;
+    };
+    ProjectionStack tiny;
+    tiny.geometry = VolumeGeometry::centered(8, 1.0);
+    tiny.matrices.assign(1, stack.matrices[0]);
+    tiny.images.assign(1, synth_projection_image(16, 16, parse_field_spec("ramp")));
+    Volume nanvol(tiny.geometry);
+    nanvol.voxels[37] = std::nanf("");
+    const bool v_nan = raises_validation([&] { conebeam_b200::reconstruct(nanvol, tiny); }) &&
+                       raises_validation([&] {
+                           conebeam_b200::backproject(nanvol, tiny.images[0], tiny.matrices[0]);
+                       }) &&
+                       std::isnan(nanvol.voxels[37]) && nanvol.voxels[36] == 0.0f;
+    Volume shortvol(tiny.geometry);
+    shortvol.voxels.resize(100);
+    const bool v_short = raises_validation([&] { conebeam_b200::reconstruct(shortvol, tiny); });
+    ProjectionStack padded = tiny;
+    padded.images[0].pad_du = -2;
+    Volume pv(tiny.geometry);
+    const bool v_pad = raises_validation([&] { conebeam_b200::reconstruct(pv, padded); }) &&
+                       raises_validation([&] {
+                           conebeam_b200::backproject(pv, padded.images[0], padded.matrices[0]);
+                       });
+    std::printf("validation nan %d short %d padded %d\n", v_nan, v_short, v_pad);
+    return (hr == 0xab67551f9fba3780ull && hg == hr && h1 == hr && threw && v_nan && v_short &&
+            v_pad)
+               ? 0
+               : 1;
 }

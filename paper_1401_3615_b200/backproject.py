@@ -130,6 +130,16 @@ def reconstruct(vol: Volume, stack: ProjectionStack, options: Optional[Options] 
     return st.to_dict()
 
 
+def _check_sizes(voxels: np.ndarray, geometry: VolumeGeometry, n_mats: int, n_imgs: int) -> None:
+    # the library trusts the pointers it is given: L^3 voxels are uploaded and
+    # written back, one matrix is read per image (Volume::validate and
+    # ProjectionStack::validate, proj/src/dataset.cpp:131-151)
+    if voxels.size != int(geometry.edge_voxels) ** 3:
+        raise ValidationError("Volume: voxel buffer length != L^3")
+    if n_mats != n_imgs:
+        raise ValidationError("ProjectionStack: images and matrices differ in length")
+
+
 def reconstruct_arrays(voxels: np.ndarray, geometry: VolumeGeometry, images: np.ndarray,
                        matrices: np.ndarray, options: Optional[Options] = None) -> dict:
     """Array-level reconstruct without validation scans (bench e2e leg):
@@ -140,6 +150,7 @@ def reconstruct_arrays(voxels: np.ndarray, geometry: VolumeGeometry, images: np.
     if images.dtype != np.float32 or not images.flags.c_contiguous or images.ndim != 3:
         raise ValidationError("images must be C-contiguous float32 (N, H, W)")
     m = validate_matrices(matrices)
+    _check_sizes(voxels, geometry, m.shape[0], images.shape[0])
     opt = options or Options()
     oc, _keep = opt.to_c()
     g = geometry_c(geometry)
@@ -165,8 +176,7 @@ def reconstruct_images(voxels: np.ndarray, geometry: VolumeGeometry, images: Seq
         if a.dtype != np.float32 or not a.flags.c_contiguous or a.shape != (h, w):
             raise ValidationError("images must be C-contiguous float32 (H, W) arrays of one shape")
     m = validate_matrices(matrices)
-    if m.shape[0] != len(imgs):
-        raise ValidationError("one matrix per image required")
+    _check_sizes(voxels, geometry, m.shape[0], len(imgs))
     ptrs = (C.c_void_p * len(imgs))(*[a.ctypes.data for a in imgs])
     oc, _keep = (options or Options()).to_c()
     st = _lib.RunStatsC()

@@ -677,6 +677,10 @@ cbb_status cbb_session_create(const cbb_volume_geometry* geometry, int32_t width
         auto s = std::make_unique<cbb_session_s>();
         s->t0 = std::chrono::steady_clock::now();
         s->pipe.init(*geometry, width, height, opt, initial_volume);
+        // Volume::validate now (proj/src/dataset.cpp:146-151), not at the
+        // first finish: a session over a non-finite volume is never created
+        if (initial_volume && !opt.volume_is_zero)
+            s->pipe.check_errors(false);
         *out = s.release();
     });
 }

@@ -93,11 +93,11 @@ void launch_pack(const float* raw, int W, int H, int count, void* packed, cudaSt
     launch_pack_band(raw, 0, H, (long long)W * H, W, H, count, packed, RowBand::full(H), st, err);
 }
 
-void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st) {
+void launch_check_finite(const float* v, long long n, int* err, cudaStream_t st, int bit = 2) {
     if (n <= 0)
         return;
     const long long blocks = std::min<long long>(148 * 4, (n / 4 + 255) / 256 + 1);
-    check_finite<<<(unsigned)blocks, 256, 0, st>>>(v, n, err);
+    check_finite<<<(unsigned)blocks, 256, 0, st>>>(v, n, err, bit);
     CK(cudaGetLastError());
     ++g_launches;
 }

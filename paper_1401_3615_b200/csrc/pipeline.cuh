@@ -337,17 +337,23 @@ struct Pipeline {
             w->d_vol = static_cast<float*>(
                 DevicePool::get().alloc(w->device, std::max<size_t>(slab, 1) * sizeof(float)));
             w->d_err = static_cast<int*>(DevicePool::get().alloc(w->device, sizeof(int)));
-            CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->compute));
+            // on the copy stream: the volume check below sets bit 4 there, and
+            // the compute stream waits for c_end before its first kernel
+            CK(cudaMemsetAsync(w->d_err, 0, sizeof(int), w->copy));
             const size_t cbytes = sizeof(unsigned long long) * kCounterSlots;
             w->d_counters = static_cast<unsigned long long*>(
                 DevicePool::get().alloc(w->device, cbytes));
             CK(cudaMemsetAsync(w->d_counters, 0, cbytes, w->compute));
             w->count_culled = opt.count_culled != 0;
             CK(cudaEventRecord(w->c_beg, w->copy));
-            if (initial_volume && !opt.volume_is_zero)
+            if (initial_volume && !opt.volume_is_zero) {
                 xfer.upload(w->d_vol, initial_volume + plane * w->z_begin, slab * sizeof(float),
                             w->copy, w->xfer_ev);
-            else
+                // Volume::validate (proj/src/dataset.cpp:146-151, called by
+                // backproject_reference, kernel_ref.cpp:7): a non-finite voxel
+                // is reported as CBB_ERR_INVALID before anything is written back
+                launch_check_finite(w->d_vol, (long long)slab, w->d_err, w->copy, 4);
+            } else
                 CK(cudaMemsetAsync(w->d_vol, 0, slab * sizeof(float), w->copy));
             CK(cudaEventRecord(w->c_end, w->copy));
             CK(cudaStreamWaitEvent(w->compute, w->c_end, 0));
@@ -772,8 +778,12 @@ struct Pipeline {
             CK(cudaMemcpy(&e, w->d_err, sizeof(int), cudaMemcpyDeviceToHost));
             err_any |= e;
         }
+        // the reference validates the images (stack.validate) before the
+        // volume (backproject_reference), kernel_ref.cpp:6-7, 33
         if (err_any & 2) // ProjectionImage::validate (proj/src/dataset.cpp:123-129)
             fail(CBB_ERR_INVALID, "ProjectionImage contains non-finite values");
+        if (err_any & 4) // Volume::validate (proj/src/dataset.cpp:146-151)
+            fail(CBB_ERR_INVALID, "Volume contains non-finite values");
         if (err_any & 1)
             fail(CBB_ERR_GEOMETRY, "backprojection hit a voxel with w == 0");
     }

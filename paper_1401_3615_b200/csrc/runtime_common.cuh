@@ -113,6 +113,9 @@ cbb_options resolve_options(const cbb_options* o) {
         fail(CBB_ERR_INVALID, "options: unknown mode %d", r.mode);
     if (r.num_gpus < 0)
         fail(CBB_ERR_INVALID, "options: num_gpus must be >= 0");
+    // device_ids has no length of its own: num_gpus gives it
+    if (r.device_ids && r.num_gpus == 0)
+        fail(CBB_ERR_INVALID, "options: device_ids needs num_gpus > 0 (its length)");
     if (r.slab_begin < 0 || r.slab_end < 0 || (r.slab_end != 0 && r.slab_end <= r.slab_begin))
         fail(CBB_ERR_INVALID, "options: bad slab [%d, %d)", r.slab_begin, r.slab_end);
     if (r.ramp_filter && !(r.filter_pixel_mm > 0.0 && std::isfinite(r.filter_pixel_mm)))
@@ -189,7 +192,10 @@ bool projection_is_safe(const double* a, const cbb_volume_geometry& g, int z_beg
         const double w = wx * a[2] + wy * a[5] + wz * a[8] + a[11];
         const double scale = std::fabs(wx * a[2]) + std::fabs(wy * a[5]) +
                              std::fabs(wz * a[8]) + std::fabs(a[11]);
-        if (!(w > 1e-4 * scale) || !(w >= 0x1p-7) || !(w <= 0x1p7))
+        // [2^-20, 2^20]: the range the kernel's FCHK-free divisions are proven
+        // for (bp_kernels.cuh, kBigBits); calibrated mm-scaled matrices with
+        // w ~ 500-1500 stay on the fast kernels
+        if (!(w > 1e-4 * scale) || !(w >= 0x1p-20) || !(w <= 0x1p20))
             return false;
         if (!(std::fabs(u / w) < 1e8) || !(std::fabs(v / w) < 1e8))
             return false;

@@ -91,6 +91,68 @@ def test_cpp_adapter_with_reference_types(cuda):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "reference ab67551f9fba3780 b200 ab67551f9fba3780" in out.stdout
+    assert "validation nan 1 short 1 padded 1" in out.stdout
+
+
+@pytest.mark.parametrize("where", [0, 7777, -1])
+def test_c_abi_rejects_non_finite_voxels(cuda, where):
+    """Volume::validate (proj/src/dataset.cpp:146-151, run by
+    backproject_reference, kernel_ref.cpp:7) at the C ABI itself: every
+    host-pointer entry point given a volume with one NaN / Inf voxel returns
+    CBB_ERR_INVALID (status 1, the reference's validation_error) with the
+    reference's message, and leaves the caller's volume untouched. The
+    Python wrappers' own host-side validation is bypassed."""
+    import ctypes as C
+
+    from paper_1401_3615_b200 import _lib
+    from paper_1401_3615_b200.backproject import geometry_c
+
+    g, mats, imgs, vol0, _ = load_golden("mini_c0.npz")
+    L = g.edge_voxels
+    bad = vol0.copy()
+    bad.reshape(-1)[where] = np.nan if where != 7777 else np.inf
+    lib = _lib.lib()
+    gc = geometry_c(g)
+    imgs = np.ascontiguousarray(imgs)
+    m = np.ascontiguousarray(mats, np.float64)
+    N, H, W = imgs.shape
+
+    def expect_invalid(status, v):
+        assert status == 1, status
+        assert lib.cbb_last_error().decode() == "Volume contains non-finite values"
+        assert bits_equal(v, bad)
+
+    for ids in ([0], [0, 0]):
+        oc, _keep = pkg.Options(device_ids=ids, batch=8).to_c()
+        v = bad.copy()
+        expect_invalid(lib.cbb_reconstruct(v.ctypes.data, C.byref(gc), imgs.ctypes.data, W, H, N,
+                                           m.ctypes.data, C.byref(oc), None), v)
+        ptrs = (C.c_void_p * N)(*[imgs[i].ctypes.data for i in range(N)])
+        v = bad.copy()
+        expect_invalid(lib.cbb_reconstruct_images(v.ctypes.data, C.byref(gc), ptrs, W, H, N,
+                                                  m.ctypes.data, C.byref(oc), None), v)
+        h = C.c_void_p()
+        expect_invalid(lib.cbb_session_create(C.byref(gc), W, H, bad.ctypes.data, C.byref(oc),
+                                              C.byref(h)), bad)
+        assert not h.value
+    v = bad.copy()
+    expect_invalid(lib.cbb_backproject(v.ctypes.data, C.byref(gc), imgs[0].ctypes.data, W, H,
+                                       m.ctypes.data), v)
+    # volume_is_zero: the caller promised zeros, nothing is read or checked
+    oc, _keep = pkg.Options(num_gpus=1, volume_is_zero=True).to_c()
+    v = bad.copy()
+    assert lib.cbb_reconstruct(v.ctypes.data, C.byref(gc), imgs.ctypes.data, W, H, N,
+                               m.ctypes.data, C.byref(oc), None) == 0
+    # a bad image is reported first, as reconstruct_reference validates the
+    # stack before the volume (kernel_ref.cpp:33)
+    badimg = imgs.copy()
+    badimg[3, 5, 5] = np.nan
+    oc, _keep = pkg.Options(num_gpus=1).to_c()
+    v = bad.copy()
+    assert lib.cbb_reconstruct(v.ctypes.data, C.byref(gc), badimg.ctypes.data, W, H, N,
+                               m.ctypes.data, C.byref(oc), None) == 1
+    assert lib.cbb_last_error().decode() == "ProjectionImage contains non-finite values"
+    assert L > 0
 
 
 def test_per_projection_entry_point(cuda):
@@ -602,10 +664,10 @@ def test_1024_volumes_planes_bitwise(cuda, oracle, cid, count):
         assert bits_equal(v[z0:z0 + 1], slab), f"config {cid} plane {z0}"
 
 
-@pytest.mark.parametrize("scale_exp", [105, -75, 0])
+@pytest.mark.parametrize("scale_exp", [105, 90, -75, 0])
 def test_extreme_pixel_magnitudes_take_the_exact_fallback(cuda, oracle, scale_exp):
     """The fast correctly-rounded weight division is proven for nonzero
-    |val| in [2^-60, 2^100]. Projections scaled by 2^105 (flagged per
+    |val| in [2^-60, 2^86). Projections scaled by 2^105 or 2^90 (flagged per
     projection by pack_quads' metadata word) or 2^-75 (caught by the kernel's
     minimum tracking) must take the IEEE-division fallback and stay bitwise
     equal to the reference; mixed with ordinary projections."""
@@ -621,6 +683,28 @@ def test_extreme_pixel_magnitudes_take_the_exact_fallback(cuda, oracle, scale_ex
     for ids in ([0], [0, 0]):
         v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=8)
         assert bits_equal(v, ref), (scale_exp, ids)
+
+
+@pytest.mark.parametrize("mscale", [1000.0, 2.0 ** -15, 2.0 ** 19])
+def test_scaled_matrices_stay_on_the_fast_kernels(cuda, oracle, mscale):
+    """Calibrated matrices are often not normalised to w ~ 1 (mm-scaled P has
+    w ~ 500-1500). The fast kernels' divisions are proven for w in
+    [2^-20, 2^20] (runtime_common.cuh: projection_is_safe), so such stacks
+    run unguarded and stay bitwise equal to the reference, mixed with an
+    ordinary pixel range and with pixels near the 2^86 numerator bound."""
+    cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=40, num_projections=20)
+    g, mats, imgs_t = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=10)
+    imgs = imgs_t.numpy().copy()
+    mats = mats * mscale
+    for big in (False, True):
+        if big:
+            imgs[3] = (imgs[3].astype(np.float64) * 2.0 ** 80).astype(np.float32)
+        ref = np.zeros((40,) * 3, np.float32)
+        assert oracle.reconstruct(ref, g, imgs, mats) == 0
+        for ids in ([0], [0, 0]):
+            v, st = gpu_reconstruct(g, mats, imgs, np.zeros_like(ref), device_ids=ids, batch=8)
+            assert st["guarded_batches"] == 0, (mscale, ids)
+            assert bits_equal(v, ref), (mscale, big, ids)
 
 
 @pytest.mark.parametrize("name", ["mini_c0.npz", "orthographic.npz"])
@@ -735,6 +819,7 @@ def test_plain_c_example_runs_on_the_gpu(cuda, tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "voxel updates" in out.stdout
+    assert 'nan voxel: status 1 "Volume contains non-finite values" (volume unchanged)' in out.stdout
 
 
 def test_concurrent_calls_from_host_threads(cuda, oracle):

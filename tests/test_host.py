@@ -335,4 +335,25 @@ def test_abi_rejects_invalid_inputs_before_touching_the_gpu():
     assert call(opt={"ramp_filter": 1, "filter_pixel_mm": 0.0})[0] == 1
     assert call(v=None)[0] == 1 and "null" in call(v=None)[1]
     assert call(im=None)[0] == 1
+    ids = (C.c_int32 * 1)(0)
+    assert call(opt={"device_ids": C.cast(ids, C.POINTER(C.c_int32))}) == (
+        1, "options: device_ids needs num_gpus > 0 (its length)")
     assert np.all(vol == 7.0)
+
+
+def test_array_entry_points_check_sizes_before_the_library():
+    """reconstruct_arrays / reconstruct_images hand raw pointers to the C ABI,
+    which reads one matrix per image and L^3 voxels: mismatched sizes raise
+    ValidationError first."""
+    g = pkg.VolumeGeometry.centered(8, 1.0)
+    imgs = np.zeros((3, 4, 5), np.float32)
+    mats = np.zeros((3, 12))
+    mats[:, 0] = mats[:, 4] = mats[:, 11] = 1.0
+    with pytest.raises(pkg.ValidationError, match="L\\^3"):
+        pkg.reconstruct_arrays(np.zeros(100, np.float32), g, imgs, mats)
+    with pytest.raises(pkg.ValidationError, match="differ in length"):
+        pkg.reconstruct_arrays(np.zeros((8, 8, 8), np.float32), g, imgs, mats[:2])
+    with pytest.raises(pkg.ValidationError, match="L\\^3"):
+        pkg.reconstruct_images(np.zeros(7, np.float32), g, list(imgs), mats)
+    with pytest.raises(pkg.ValidationError, match="differ in length"):
+        pkg.reconstruct_images(np.zeros((8, 8, 8), np.float32), g, list(imgs), mats[:1])
