@@ -52,6 +52,14 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the other-mode and 1024^3 secondary measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config4", action="store_true",
+                    help="skip the config-4 (1440 x 1536^2 -> 1024^3) secondary")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle check of the timed run's volume")
+    ap.add_argument("--parity-stride", type=int, default=32,
+                    help="oracle-check every k-th z-plane (plus the last) of the timed volume")
+    ap.add_argument("--ref-projections", type=int, default=0,
+                    help="--impl reference: projections per step (0 = all, the stated config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU seconds for the cpu_baseline sample")
     return ap.parse_args()
@@ -196,20 +204,28 @@ def run_reference_arm(args):
 
     cfg = synth.CONFIGS[args.config]
     total_steps = args.steps + args.warmup
-    budget = 150.0  # seconds for the whole run
-    n, cores = size_cpu_sample(cfg, budget / max(total_steps, 1))
+    # every step is the whole stated workload (all projections of the config
+    # into the full volume: same_config with our arm); --ref-projections
+    # bounds it for quick manual runs only
+    n = cfg.num_projections if args.ref_projections <= 0 else min(args.ref_projections,
+                                                                   cfg.num_projections)
     g, mats, imgs = cpu_inputs(cfg, n)
-    vals, secs = [], []
+    vals, secs, pre = [], [], []
     kind = "port"
+    cores = os.cpu_count() or 1
     for i in range(total_steps):
         gups, st, kind, cores = time_reference_cpu(cfg, n, g, mats, imgs)
         if i >= args.warmup:
             vals.append(gups)
             secs.append(st["kernel_seconds"])
+            pre.append(st.get("precompute_seconds", 0.0))
     value = statistics.median(vals)
-    sample = (f"config {args.config} volume {cfg.edge_voxels}^3 x first {n} of "
-              f"{cfg.num_projections} projections per step; reconstruct_optimized defaults "
-              f"(lanes 16, chunk 262, clip+pad), kernel_seconds; full-basis updates")
+    full_incl = cfg.edge_voxels ** 3 * n / (statistics.median(secs) + statistics.median(pre)) / 1e9
+    sample = (f"config {args.config}: all {n} of {cfg.num_projections} projections into the "
+              f"{cfg.edge_voxels}^3 volume every step; reconstruct_optimized defaults "
+              f"(lanes 16, chunk 262, clip+pad), its kernel_seconds (clip/pad precompute of "
+              f"{statistics.median(pre):.2f} s per call excluded, as the reference bench does "
+              f"by default); full-basis updates")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GUp/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -219,7 +235,8 @@ def run_reference_arm(args):
                    "projections": cfg.num_projections, "detector": [cfg.width, cfg.height],
                    "sampled_projections": n, "l2": "inputs larger than L2"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GUp/s", "cores": cores,
-                         "kind": kind, "sample": sample},
+                         "kind": kind, "sample": sample,
+                         "full_basis_incl_precompute": round(full_incl, 4)},
         "e2e": {"value": round(value, 4), "unit": "GUp/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -419,6 +436,16 @@ def run_ours(args):
             # computes (the full basis includes the culled, provably-zero ones)
             line["roofline"]["frac_on_computed_updates"] = round(
                 line["roofline"]["frac"] * (1.0 - line["culled_fraction"]), 4)
+    if rank == 0 and world == 1 and not args.no_parity:
+        line["parity"] = parity_entry(c)
+    if world == 1 and not args.no_secondary:
+        c.ms_step = ms_step
+        line.setdefault("secondary", []).append(filter_entry(c))
+        c.vol = None
+        vol = None
+        torch.cuda.empty_cache()
+        if not args.no_config4:
+            line["secondary"].append(config4_entry(c))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_entry(c)
     if rank == 0:
@@ -640,8 +667,236 @@ def e2e_entries(c):
             batch=args.batch, mode=mode, num_gpus=1, device_ids=[local],
             volume_is_zero=True, count_culled=True))
         out["culled_fraction"] = round(cst["culled_fraction"], 4)
+        # the host API's volume against the device-resident run's (same bits
+        # expected: one arithmetic, any batching / staging / resident tail)
+        vt = torch.from_numpy(buf[z0:z1]).to(dev)
+        dff = pkg.compare_volumes_device(vt, c.vol)
+        out["e2e"]["bitwise_different_vs_value_volume"] = int(dff["bitwise_different"])
+        del vt
+        out["e2e_adapter"] = e2e_adapter_entry(c, imgs_np)
     del vol_h
     return out
+
+
+def e2e_adapter_entry(c, imgs_src):
+    """The drop-in's own host path, as the C++ adapter drives it
+    (include/conebeam_b200.hpp reconstruct -> cbb_reconstruct_images): one
+    PAGEABLE buffer per projection (the reference's ProjectionStack holds one
+    std::vector<float> per image, dataset.hpp:15-60) and a NON-ZERO pageable
+    volume that is uploaded, accumulated into and downloaded (vol +=,
+    kernel_ref.cpp:32-38) -- no pinned inputs, no volume_is_zero."""
+    import numpy as np
+
+    pkg, args, g, mats, L, n, H, W = c.pkg, c.args, c.g, c.mats, c.L, c.n, c.H, c.W
+    parts = [np.array(imgs_src[i]) for i in range(n)]  # n separate pageable buffers
+    vol = np.full((L, L, L), 0.25, np.float32)          # pageable, non-zero
+    opt = pkg.Options(batch=args.batch, mode=c.mode, num_gpus=1, device_ids=[c.local])
+    pkg.reconstruct_images(vol, g, parts, mats, opt)    # warm-up
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        pkg.reconstruct_images(vol, g, parts, mats, opt)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    del parts, vol
+    return {"value": round(L ** 3 * n / t / 1e9, 3), "unit": "GUp/s", "seconds": round(t, 4),
+            "h2d_bytes_per_step": int(n * H * W * 4 + mats.nbytes + L ** 3 * 4),
+            "d2h_bytes_per_step": int(L ** 3 * 4),
+            "path": "cbb_reconstruct_images (the C++ adapter's call): pageable per-image "
+                    "buffers, non-zero pageable volume uploaded + accumulated + downloaded"}
+
+
+def filter_entry(c):
+    """FDK ramp-filter stage (upstream of the reference's
+    input): raw line integrals of the same scan, (a) the filter alone on
+    device-resident data (cbb_ramp_filter_device, CUDA events), with its
+    roofline, and (b) end to end through cbb_reconstruct with
+    options.ramp_filter from pinned host line integrals."""
+    import numpy as np
+
+    pkg, torch, dev, args, cfg = c.pkg, c.torch, c.dev, c.args, c.cfg
+    g, mats, L, n, H, W, stream = c.g, c.mats, c.L, c.n, c.H, c.W, c.stream
+    from paper_1401_3615_b200 import synth
+
+    _, _, raw = synth.make_inputs(cfg, device=dev, chunk=16, filtered=False)
+    out = torch.empty_like(raw)
+    pkg.ramp_filter_device(raw, out, cfg.pixel_mm, stream)  # warm-up (plans, spectrum)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    a.record(stream)
+    for _ in range(reps):
+        pkg.ramp_filter_device(raw, out, cfg.pixel_mm, stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    pixels = n * H * W
+    peaks, src = measured_peaks()
+    alg_bytes = 8 * pixels  # read + write one float per pixel
+    res = {"workload": cfg.name, "stage": "ramp filter (Shepp-Logan, row-wise, float64)",
+           "ms_per_stack": round(ms, 3), "share_of_step": round(ms / c.ms_step, 4),
+           "roofline": {"bound": "hbm", "achieved": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
+                        "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                        "frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peaks.get("hbm_gbs"), 4),
+                        "algorithmic_bytes": int(alg_bytes), "peak_source": src}}
+    impl = pkg.ramp_filter_info() if hasattr(pkg, "ramp_filter_info") else None
+    if impl:
+        res["implementation"] = impl
+    # e2e: raw line integrals from pinned host memory -> filtered on the GPU ->
+    # back-projected -> host volume
+    raw_h = raw.cpu().pin_memory()
+    del raw, out
+    torch.cuda.empty_cache()
+    raw_np = raw_h.numpy()
+    vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
+    buf = vol_h.numpy()
+    opt = pkg.Options(batch=args.batch, mode=c.mode, num_gpus=1, device_ids=[c.local],
+                      volume_is_zero=True, ramp_filter_pixel_mm=cfg.pixel_mm)
+    pkg.reconstruct_arrays(buf, g, raw_np, mats, opt)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        pkg.reconstruct_arrays(buf, g, raw_np, mats, opt)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    vt = torch.from_numpy(buf).to(dev)
+    d = pkg.compare_volumes_device(vt, c.vol)
+    res["e2e_filtered"] = {
+        "value": round(L ** 3 * n / t / 1e9, 3), "unit": "GUp/s", "seconds": round(t, 4),
+        "h2d_bytes_per_step": int(raw_np.nbytes + mats.nbytes), "d2h_bytes_per_step": L ** 3 * 4,
+        "vs_prefiltered_volume": {k: d[k] for k in ("rel_l2", "max_abs_over_range")},
+        "path": "cbb_reconstruct, options.ramp_filter, pinned raw line integrals"}
+    del vt, raw_h, vol_h
+    torch.cuda.empty_cache()
+    return res
+
+
+def config4_entry(c):
+    """BASELINE config 4 on this GPU (the single-GPU leg of its 8-GPU run):
+    1440 x 1536^2 projections of a 360-degree scan into a 1024^3 volume,
+    batches of 16 as BASELINE states. Device-resident value with its roofline,
+    culled fraction, and e2e through cbb_reconstruct from pinned host memory
+    (13.6 GB in, 4.3 GB out)."""
+    pkg, torch, dev, args = c.pkg, c.torch, c.dev, c.args
+    from paper_1401_3615_b200 import synth
+
+    cfg = synth.CONFIGS[4]
+    pkg.release_cached_memory()  # earlier pipelines' cached device buffers
+    torch.cuda.empty_cache()
+    g, mats, imgs = synth.make_inputs(cfg, device=dev, chunk=16)
+    L = g.edge_voxels
+    n, H, W = imgs.shape
+    nb = pkg.packed_layout(W, H)[2]
+    packed = torch.empty(n * nb, dtype=torch.uint8, device=dev)
+    vol = torch.empty((L, L, L), dtype=torch.float32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = c.stream
+    res = {"workload": cfg.name, "edge_voxels": L, "projections": n, "detector": [W, H],
+           "mode": args.mode}
+    for batch in (16, 32):
+        opt = pkg.Options(batch=batch, mode=c.mode)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+        def step(rec=False):
+            vol.zero_()
+            if rec:
+                ev[0].record(stream)
+            pkg.pack_device(imgs, packed, stream)
+            if rec:
+                ev[1].record(stream)
+            pkg.backproject_device(vol, g, 0, L, packed, W, H, n, mats, opt, err, stream)
+            if rec:
+                ev[2].record(stream)
+        step()
+        torch.cuda.synchronize()
+        bp, pk = [], []
+        for _ in range(2):
+            step(True)
+            torch.cuda.synchronize()
+            pk.append(ev[0].elapsed_time(ev[1]))
+            bp.append(ev[1].elapsed_time(ev[2]))
+        ms = statistics.mean(pk) + statistics.mean(bp)
+        nl = (n + batch - 1) // batch
+        launch_ms = statistics.mean(bp) / nl
+        upd = L ** 3 * (n / nl)
+        peaks, _ = measured_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        frac = upd * OPS_PER_UPDATE / (launch_ms * 1e-3) / (nsm * 128 * sm_max * 1e6)
+        res[f"batch{batch}"] = {"value": round(L ** 3 * n / (ms * 1e-3) / 1e9, 3),
+                                "unit": "GUp/s", "ms_per_step": round(ms, 2),
+                                "pack_ms": round(statistics.mean(pk), 2),
+                                "roofline_frac": round(frac, 4)}
+    if int(err.item()) != 0:
+        res["error_flag"] = int(err.item())
+    res["value"] = res["batch16"]["value"]
+    imgs_h = imgs.cpu().pin_memory()
+    del imgs, packed, vol
+    torch.cuda.empty_cache()
+    imgs_np = imgs_h.numpy()
+    vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
+    buf = vol_h.numpy()
+    opt = pkg.Options(batch=16, mode=c.mode, num_gpus=1, device_ids=[c.local],
+                      volume_is_zero=True)
+    cst = pkg.reconstruct_arrays(buf, g, imgs_np, mats, pkg.Options(
+        batch=16, mode=c.mode, num_gpus=1, device_ids=[c.local], volume_is_zero=True,
+        count_culled=True))
+    res["culled_fraction"] = round(cst["culled_fraction"], 4)
+    ts = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        st = pkg.reconstruct_arrays(buf, g, imgs_np, mats, opt)
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    res["e2e"] = {"value": round(L ** 3 * n / t / 1e9, 3), "unit": "GUp/s",
+                  "seconds": round(t, 4), "h2d_bytes_per_step": int(imgs_np.nbytes + mats.nbytes),
+                  "d2h_bytes_per_step": L ** 3 * 4, "guarded_batches": st["guarded_batches"],
+                  "path": "cbb_reconstruct (C ABI), pinned host buffers, batch 16"}
+    del imgs_h, vol_h, imgs_np, buf
+    pkg.release_cached_memory()
+    torch.cuda.empty_cache()
+    return res
+
+
+def parity_entry(c):
+    """The timed run's own volume (the last timed step's output, still on the
+    device) against the oracle, outside the timed region: every
+    --parity-stride-th z-plane plus the last, all projections, recomputed by
+    oracle_reconstruct_planes on the host cores and cached under a content
+    hash of the inputs -- the reference bench scores every benchmarked volume
+    against a reference volume cached by stack hash the same way
+    (proj/src/bench.cpp:194-243)."""
+    import numpy as np
+
+    import oracle as O
+
+    args, g, mats, L = c.args, c.g, c.mats, c.L
+    try:
+        planes = np.array(sorted(set(range(c.z0, c.z1, max(1, args.parity_stride))) |
+                                 {c.z1 - 1}))
+        host = c.imgs.cpu().numpy()
+        ref, secs, hit = O.reference_planes(g, planes, host, mats)
+        del host
+        got = c.vol[c.torch.as_tensor(planes - c.z0, device=c.dev)].cpu().numpy()
+        d = got.astype(np.float64) - ref.astype(np.float64)
+        rng = float(ref.max()) - float(ref.min())
+        rel = float(np.linalg.norm(d) / max(np.linalg.norm(ref.astype(np.float64)), 1e-300))
+        mar = float(np.abs(d).max() / rng) if rng > 0 else float(np.abs(d).max())
+        return {
+            "vs": "oracle (C restatement of reconstruct_reference, pinned to the reference's "
+                  "golden hash and to the reference itself)",
+            "volume": "the timed run's own output (last timed step)",
+            "planes_checked": int(planes.size), "of_planes": int(c.z1 - c.z0),
+            "plane_stride": int(args.parity_stride),
+            "voxels_checked": int(got.size),
+            "bitwise_different": int(np.count_nonzero(got.view(np.uint32) !=
+                                                      ref.view(np.uint32))),
+            "rel_l2": rel, "max_abs_over_range": mar,
+            "within_north_star_tolerance": bool(rel <= 1e-5 and mar <= 1e-4),
+            "oracle_seconds": round(secs, 2), "oracle_cache_hit": bool(hit),
+            "oracle_threads": os.cpu_count()}
+    except Exception as e:  # reported, never silently dropped
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def cpu_baseline_entry(c):

@@ -291,6 +291,161 @@ int oracle_reconstruct_slab(float *vol_slab, int L, double voxel_mm, double orig
     return status;
 }
 
+/* ---- arbitrary z-planes, cache-tiled (large-volume parity checks) --------
+ * reconstruct_reference restricted to a list of z-planes. Work units are
+ * tiles of TILE_LINES consecutive y-lines of one plane; a unit applies every
+ * projection in order to all its lines before the next projection, so the
+ * detector footprint of the tile stays in cache across its lines. Each voxel
+ * still receives its projections one by one in ascending order with the
+ * arithmetic of sample_one, so the result is bitwise that of the reference
+ * for every tiling and thread count. Units are handed out dynamically. */
+#define TILE_LINES 8
+
+struct planes_job {
+    float *out;            /* nplanes x L x L */
+    const int *planes;
+    int nplanes, L;
+    float O, MM;
+    const float *imgs;
+    int width, height, count;
+    const double *mats;
+    int units;
+    int *next;             /* shared unit counter */
+    int *status;           /* shared status */
+};
+
+static void *planes_worker(void *arg) {
+    struct planes_job *j = (struct planes_job *)arg;
+    const size_t pix = (size_t)j->width * j->height;
+    const int L = j->L;
+    const int tiles_per_plane = (L + TILE_LINES - 1) / TILE_LINES;
+    for (;;) {
+        const int u = __atomic_fetch_add(j->next, 1, __ATOMIC_RELAXED);
+        if (u >= j->units || __atomic_load_n(j->status, __ATOMIC_RELAXED) != ORACLE_OK)
+            break;
+        const int pi = u / tiles_per_plane;
+        const int y0 = (u % tiles_per_plane) * TILE_LINES;
+        const int y1 = y0 + TILE_LINES < L ? y0 + TILE_LINES : L;
+        const int z = j->planes[pi];
+        const float wz = j->O + z * j->MM;
+        for (int p = 0; p < j->count; ++p) {
+            float a[12];
+            cast_matrix(j->mats + 12 * (size_t)p, a);
+            const float *img = j->imgs + pix * p;
+            int zero_w = 0;
+            for (int y = y0; y < y1; ++y) {
+                const float wy = j->O + y * j->MM;
+                float *line = j->out + ((size_t)pi * L + y) * L;
+                for (int x = 0; x < L; ++x) {
+                    const float wx = j->O + x * j->MM;
+                    line[x] += sample_one(img, j->width, j->height, a, wx, wy, wz, &zero_w);
+                    if (zero_w) {
+                        __atomic_store_n(j->status, ORACLE_ERR_GEOMETRY, __ATOMIC_RELAXED);
+                        return NULL;
+                    }
+                }
+            }
+        }
+    }
+    return NULL;
+}
+
+/* out: nplanes x L x L floats, accumulated (+=) like the volume planes
+ * planes[0..nplanes) of reconstruct_reference. */
+int oracle_reconstruct_planes(float *out, int L, double voxel_mm, double origin_mm,
+                              const int *planes, int nplanes, const float *imgs, int width,
+                              int height, int count, const double *mats, int threads) {
+    if (!out || !planes || !imgs || !mats || L < 1 || nplanes < 1 || width < 1 || height < 1 ||
+        count < 1)
+        return ORACLE_ERR_INVALID;
+    for (int i = 0; i < nplanes; ++i)
+        if (planes[i] < 0 || planes[i] >= L)
+            return ORACLE_ERR_INVALID;
+    if (threads < 1)
+        threads = 1;
+    int next = 0, status = ORACLE_OK;
+    struct planes_job job = {out, planes, nplanes, L, (float)origin_mm, (float)voxel_mm, imgs,
+                             width, height, count, mats,
+                             nplanes * ((L + TILE_LINES - 1) / TILE_LINES), &next, &status};
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof *tids);
+    if (!tids)
+        return ORACLE_ERR_INVALID;
+    for (int t = 0; t < threads; ++t)
+        pthread_create(&tids[t], NULL, planes_worker, &job);
+    for (int t = 0; t < threads; ++t)
+        pthread_join(tids[t], NULL);
+    free(tids);
+    return status;
+}
+
+/* ---- content hash for the oracle-volume cache ------------------------------
+ * The reference's bench caches its reference volume under the FNV-1a hash of
+ * the stack file (proj/src/bench.cpp:194-214). Stacks here are up to 13.6 GB,
+ * so the key is FNV-1a over 64-bit words of fixed 64 MiB chunks (hashed in
+ * parallel), folded in chunk order with the total length: a different, but
+ * equally deterministic, content key. */
+#define HASH_CHUNK (64ull << 20)
+
+struct hash_job {
+    const unsigned char *data;
+    size_t n, nchunks;
+    uint64_t *out;
+    int *next;
+};
+
+static uint64_t fnv_words(const unsigned char *p, size_t n) {
+    uint64_t h = 1469598103934665603ull;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        memcpy(&w, p + i, 8);
+        h ^= w;
+        h *= 1099511628211ull;
+    }
+    for (; i < n; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+static void *hash_worker(void *arg) {
+    struct hash_job *j = (struct hash_job *)arg;
+    for (;;) {
+        const size_t c = (size_t)__atomic_fetch_add(j->next, 1, __ATOMIC_RELAXED);
+        if (c >= j->nchunks)
+            break;
+        const size_t off = c * HASH_CHUNK;
+        const size_t len = j->n - off < HASH_CHUNK ? j->n - off : HASH_CHUNK;
+        j->out[c] = fnv_words(j->data + off, len);
+    }
+    return NULL;
+}
+
+uint64_t oracle_content_hash(const void *data, size_t n, int threads) {
+    const size_t nchunks = (n + HASH_CHUNK - 1) / HASH_CHUNK;
+    uint64_t *part = (uint64_t *)calloc(nchunks ? nchunks : 1, sizeof *part);
+    if (!part)
+        return 0;
+    int next = 0;
+    struct hash_job job = {(const unsigned char *)data, n, nchunks, part, &next};
+    if (threads < 1)
+        threads = 1;
+    if ((size_t)threads > nchunks)
+        threads = nchunks ? (int)nchunks : 1;
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof *tids);
+    for (int t = 0; tids && t < threads; ++t)
+        pthread_create(&tids[t], NULL, hash_worker, &job);
+    for (int t = 0; tids && t < threads; ++t)
+        pthread_join(tids[t], NULL);
+    uint64_t h = fnv_words((const unsigned char *)part, nchunks * sizeof *part);
+    h ^= (uint64_t)n;
+    h *= 1099511628211ull;
+    free(tids);
+    free(part);
+    return h;
+}
+
 /* FNV-1a 64 over raw bytes (proj/tests/helpers.hpp:41-49). */
 uint64_t oracle_fnv1a64(const void *data, size_t n) {
     const unsigned char *p = (const unsigned char *)data;

@@ -238,13 +238,14 @@ def ramp_filter(proj, pixel_mm: float):
 
 
 def make_inputs(cfg: ScanConfig, device="cpu", out_device=None, chunk: int = 8,
-                count: int = None, pin: bool = False):
+                count: int = None, pin: bool = False, filtered: bool = True):
     """(geometry, matrices (n,12) float64 numpy, images float32 torch (n,H,W)).
 
     Images are produced chunk-wise on `device` and stored on `out_device`
     (default: same device). `count` keeps only the first projections of the
     scan (same bytes as the full scan's first `count`); `pin` places CPU
-    output in page-locked memory."""
+    output in page-locked memory; filtered=False returns the raw line
+    integrals (rounded to float32) for the GPU FDK filter stage."""
     import torch
 
     n = cfg.num_projections if count is None else min(int(count), cfg.num_projections)
@@ -256,6 +257,7 @@ def make_inputs(cfg: ScanConfig, device="cpu", out_device=None, chunk: int = 8,
     for p0 in range(0, n, chunk):
         p1 = min(n, p0 + chunk)
         li = line_integrals(mats[p0:p1], cfg.width, cfg.height, ells, device=device, chunk=chunk)
-        imgs[p0:p1] = ramp_filter(li, cfg.pixel_mm).to(torch.float32).to(out_device)
+        f = ramp_filter(li, cfg.pixel_mm) if filtered else li
+        imgs[p0:p1] = f.to(torch.float32).to(out_device)
         del li
     return cfg.geometry, mats, imgs

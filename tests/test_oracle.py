@@ -181,3 +181,44 @@ def test_reference_optimized_degenerate_options_are_the_reference(oracle):
                                           use_clip=False, use_pad=False)
     assert st["status"] == 0
     assert bits_equal(a, b)
+
+
+def test_planes_oracle_equals_full_reconstruction_and_caches(oracle, tmp_path, monkeypatch):
+    """oracle_reconstruct_planes (cache-tiled, dynamic threads; used for the
+    headline-size parity tests and bench.py's parity block) gives the same
+    bits as the reference-order oracle for any plane list, including w == 0
+    errors; the hash-keyed cache returns the same planes without recomputing
+    (proj/src/bench.cpp:194-214)."""
+    g, mats, imgs, vol0, expected = load_golden("mini_c0.npz")
+    L = g.edge_voxels
+    full = np.zeros((L, L, L), np.float32)
+    assert oracle.reconstruct(full, g, imgs, mats) == 0
+    for planes in ([0], [L - 1, 0, 3], list(range(L))):
+        for threads in (1, 3):
+            out = np.zeros((len(planes), L, L), np.float32)
+            assert oracle.reconstruct_planes(out, g, planes, imgs, mats, threads=threads) == 0
+            assert bits_equal(out, full[planes])
+    monkeypatch.setenv("CBB_ORACLE_CACHE", str(tmp_path))
+    a, secs_a, hit_a = oracle.reference_planes(g, [1, 2], imgs, mats)
+    b, secs_b, hit_b = oracle.reference_planes(g, [1, 2], imgs, mats)
+    assert not hit_a and hit_b and secs_b == 0.0
+    assert bits_equal(a, full[[1, 2]]) and bits_equal(b, a)
+    imgs2 = imgs.copy()
+    imgs2[0, 0, 0] += 1.0  # different content, different key
+    c, _, hit_c = oracle.reference_planes(g, [1, 2], imgs2, mats)
+    assert not hit_c
+    # w == 0 is reported as the geometry error (status 5)
+    bad = np.zeros((1, 12))
+    bad[0, 0] = bad[0, 4] = 1.0
+    out = np.zeros((1, L, L), np.float32)
+    assert oracle.reconstruct_planes(out, g, [0], imgs[:1], bad) == 5
+
+
+def test_content_hash_is_chunked_and_deterministic(oracle):
+    a = np.arange(3_000_001, dtype=np.float32)
+    h = oracle.content_hash(a)
+    assert h == oracle.content_hash(a.copy())
+    b = a.copy()
+    b[-1] += 1
+    assert oracle.content_hash(b) != h
+    assert oracle.content_hash(a[:-1]) != h
