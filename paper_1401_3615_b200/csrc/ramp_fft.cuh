@@ -1,0 +1,300 @@
+// ramp_fft.cuh -- hand-written sm_100a FDK ramp filter: one fused kernel per
+// stack, FP64 FFT convolution in shared memory.
+//
+// Same definition as ramp_filter.cuh (and the input generator,
+// paper_1401_3615_b200/synth.py): every detector row is linearly convolved
+// with the Shepp-Logan kernel h[n] = -2 / (pi^2 tau (4 n^2 - 1)), tau = pixel
+// pitch, in float64, and rounded to float32. The cuFFT path it replaces
+// (ramp_filter.cuh: widen rows to 4096 doubles in HBM, D2Z, spectrum
+// multiply, Z2D, narrow) moved ~130 GB through HBM for config 2's 476k rows
+// (27.7 ms, 34 % of a back-projection step; BENCH r2a). Here each row is read
+// once and written once (8 B per pixel):
+//
+//   * two rows form one complex sequence z = x1 + i x2 (zero-padded to
+//     N = 4096 >= 2W - 1, so the circular convolution equals the linear one on
+//     the W outputs); h is real and even, so its spectrum H is real and
+//     IFFT(FFT(z) H) = (x1 * h) + i (x2 * h): the two filtered rows come back
+//     as the real and imaginary parts, with no split/merge step;
+//   * the FFT is a radix-16 Stockham transform (16^3 = 4096) by 256 threads,
+//     16 points per thread in registers: pass 1 loads the rows straight from
+//     global memory (coalesced), the forward transform's last pass leaves
+//     every thread holding exactly the 16 frequencies the inverse transform's
+//     first pass needs, so the spectrum multiply and that pass happen in
+//     registers; the inverse's last pass stores the W outputs (scaled by 1/N,
+//     folded into H) straight to global memory. Shared memory (re / im double
+//     planes, one pad word per 16) carries only the 4 remaining exchanges.
+//
+// FP64 (64 lanes/clk/SM on B200) bounds it: ~370k FP64 ops per row pair.
+// Detectors wider than 2048 pixels keep the cuFFT path.
+#pragma once
+
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/conebeam_b200.h"
+
+namespace cbb {
+
+[[noreturn]] void fail(cbb_status s, const char* fmt, ...);
+void check_cuda(cudaError_t e, const char* what);
+extern thread_local uint64_t g_launches;
+
+constexpr int kRfN = 4096;                     // FFT length
+constexpr int kRfT = 256;                      // threads per FFT (N / 16)
+constexpr int kRfMaxW = 2048;                  // N >= 2W - 1
+__host__ __device__ constexpr int rf_pad(int i) { return i + (i >> 4); }
+constexpr int kRfPlane = rf_pad(kRfN);         // doubles per re / im plane
+constexpr int kRfSmemBytes = 2 * kRfPlane * 8; // 69632 B
+
+struct cd {
+    double x, y;
+};
+__device__ __forceinline__ cd operator+(cd a, cd b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cd operator-(cd a, cd b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cd cmul(cd a, cd b) {
+    return {fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+
+// DFT of 4 points in place; forward uses W4 = -i, inverse +i.
+template <bool INV>
+__device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
+    const cd t0 = a0 + a2, t1 = a0 - a2, t2 = a1 + a3, t3 = a1 - a3;
+    const cd rt3 = INV ? cd{-t3.y, t3.x} : cd{t3.y, -t3.x}; // (+-i) * t3
+    a0 = t0 + t2;
+    a2 = t0 - t2;
+    a1 = t1 + rt3;
+    a3 = t1 - rt3;
+}
+
+// v[m] *= W16^e (forward: exp(-2 pi i e / 16), inverse: conjugate), e < 16.
+template <bool INV, int E>
+__device__ __forceinline__ void w16(cd& v) {
+    constexpr double C1 = 0.92387953251128674, S1 = 0.38268343236508978;
+    constexpr double R2 = 0.70710678118654752;
+    constexpr int e = E % 16;
+    // exp(-2 pi i e/16) = cos - i sin; inverse flips the sign of sin
+    constexpr double sg = INV ? -1.0 : 1.0;
+    if (e == 0)
+        return;
+    if (e == 4) { // -i (forward) / +i (inverse)
+        v = INV ? cd{-v.y, v.x} : cd{v.y, -v.x};
+        return;
+    }
+    if (e == 8) {
+        v = cd{-v.x, -v.y};
+        return;
+    }
+    if (e == 2 || e == 6) { // (1 -+ i)/sqrt2 rotations
+        const double c = e == 2 ? R2 : -R2, s = sg * R2;
+        v = cd{fma(v.x, c, v.y * s), fma(v.y, c, -v.x * s)};
+        return;
+    }
+    const double c = (e == 1 || e == 15) ? C1 : (e == 3 || e == 13) ? S1
+                   : (e == 5 || e == 11) ? -S1 : (e == 7 || e == 9) ? -C1 : 0.0;
+    const double s0 = (e == 1 || e == 7) ? S1 : (e == 3 || e == 5) ? C1
+                    : (e == 9 || e == 15) ? -S1 : (e == 11 || e == 13) ? -C1 : 0.0;
+    const double s = sg * s0;
+    // (x + i y)(c - i s) = (x c + y s) + i (y c - x s)
+    v = cd{fma(v.x, c, v.y * s), fma(v.y, c, -v.x * s)};
+}
+
+// 16-point DFT of v[0..15] (input in natural order). Output X[k] lands in
+// v[4 (k % 4) + k / 4] (radix-4 x radix-4, n = 4 n1 + n2, k = k1 + 4 k2).
+template <bool INV>
+__device__ __forceinline__ void dft16(cd (&v)[16]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2)
+        dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]); // v[4 k1 + n2] = A[n2][k1]
+    w16<INV, 1>(v[5]);
+    w16<INV, 2>(v[6]);
+    w16<INV, 3>(v[7]);
+    w16<INV, 2>(v[9]);
+    w16<INV, 4>(v[10]);
+    w16<INV, 6>(v[11]);
+    w16<INV, 3>(v[13]);
+    w16<INV, 6>(v[14]);
+    w16<INV, 9>(v[15]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+        dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+}
+__device__ __forceinline__ constexpr int x16(int k) { return 4 * (k % 4) + k / 4; }
+
+// One Stockham pass over shared memory: read 16 points at stride 256,
+// twiddle by exp(-+2 pi i r (j % NS) / (16 NS)), DFT16, write at stride NS.
+template <bool INV, int NS, bool READ, bool WRITE>
+__device__ __forceinline__ void rf_pass(cd (&v)[16], double* re, double* im,
+                                        const double2* __restrict__ tw, int j) {
+    if (READ) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int i = rf_pad(j + r * kRfT);
+            v[r] = cd{re[i], im[i]};
+        }
+        __syncthreads(); // every read done before this pass's writes
+    }
+    if (NS > 1) {
+        // w1 = exp(-2 pi i e / 4096), e = (j % NS) * 4096 / (16 NS); w_r = w1^r
+        const double2 t = __ldg(tw + (j % NS) * (kRfN / (16 * NS)));
+        const cd w1 = INV ? cd{t.x, -t.y} : cd{t.x, t.y};
+        cd w = w1;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+            v[r] = cmul(v[r], w);
+            if (r < 15)
+                w = cmul(w, w1);
+        }
+    }
+    dft16<INV>(v);
+    if (WRITE) {
+        const int base = (j / NS) * NS * 16 + (j % NS);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = rf_pad(base + q * NS);
+            re[i] = v[x16(q)].x;
+            im[i] = v[x16(q)].y;
+        }
+        __syncthreads();
+    } else {
+        // outputs in natural order for the caller: X[j + 256 q] = v[x16(q)]
+        cd o[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            o[q] = v[x16(q)];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            v[q] = o[q];
+    }
+}
+
+// rows: `rows` rows of W floats (row-major, row r at raw + r * W); pairs of
+// rows (2p, 2p+1) per iteration; grid-stride over pairs. spec: N real
+// spectrum values of h, scaled by 1/N. tw: exp(-2 pi i e / N), e < N.
+__global__ void __launch_bounds__(kRfT, 2)
+ramp_fft_rows(const float* raw, float* out, int W, long long rows,
+              const double* __restrict__ spec, const double2* __restrict__ tw) {
+    extern __shared__ double rf_smem[];
+    double* re = rf_smem;
+    double* im = rf_smem + kRfPlane;
+    const int j = threadIdx.x;
+    const long long pairs = (rows + 1) / 2;
+    for (long long p = blockIdx.x; p < pairs; p += gridDim.x) {
+        const float* r1 = raw + (2 * p) * (long long)W;
+        const bool two = 2 * p + 1 < rows;
+        const float* r2 = r1 + W;
+        cd v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int n = j + r * kRfT;
+            const bool in = n < W;
+            v[r] = cd{in ? (double)__ldg(r1 + n) : 0.0, (in && two) ? (double)__ldg(r2 + n) : 0.0};
+        }
+        // forward: Ns = 1 (from registers), 16, 256 (ends in registers)
+        rf_pass<false, 1, false, true>(v, re, im, tw, j);
+        rf_pass<false, 16, true, true>(v, re, im, tw, j);
+        rf_pass<false, 256, true, false>(v, re, im, tw, j);
+        // spectrum multiply: thread j holds Z[j + 256 q] in v[q] -- exactly
+        // the inverse's first-pass inputs (stride N/16 = 256)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const double h = __ldg(spec + j + q * kRfT);
+            v[q] = cd{v[q].x * h, v[q].y * h};
+        }
+        rf_pass<true, 1, false, true>(v, re, im, tw, j);
+        rf_pass<true, 16, true, true>(v, re, im, tw, j);
+        rf_pass<true, 256, true, false>(v, re, im, tw, j);
+        float* o1 = out + (2 * p) * (long long)W;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int n = j + q * kRfT;
+            if (n < W) {
+                o1[n] = (float)v[q].x;
+                if (two)
+                    o1[W + n] = (float)v[q].y;
+            }
+        }
+    }
+}
+
+// spec[k] = (1/N) sum_n hc[n] cos(2 pi k n / N), hc the wrapped kernel
+// (n <= N/2: h(n), else h(n - N)); tw[e] = exp(-2 pi i e / N).
+__global__ void ramp_fft_tables(double* spec, double2* tw, int N, double tau) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N)
+        return;
+    double s = 0.0;
+    for (int n = 0; n < N; ++n) {
+        const double m = n <= N / 2 ? (double)n : (double)(n - N);
+        const double h = -2.0 / (M_PI * M_PI * tau * (4.0 * m * m - 1.0));
+        const long long e = ((long long)k * n) % N;
+        s += h * cospi(2.0 * (double)e / (double)N);
+    }
+    spec[k] = s / (double)N;
+    double sn, cs;
+    sincospi(2.0 * (double)k / (double)N, &sn, &cs);
+    tw[k] = make_double2(cs, -sn);
+}
+
+struct RampFftTables {
+    double* spec = nullptr;
+    double2* tw = nullptr;
+};
+
+class RampFftCache {
+  public:
+    static RampFftCache& get() {
+        static RampFftCache c;
+        return c;
+    }
+    // tables for (device, tau); built once on stream st (synchronously)
+    RampFftTables tables(int device, double tau, cudaStream_t st) {
+        std::lock_guard<std::mutex> lk(mu_);
+        auto key = std::make_tuple(device, tau);
+        auto it = map_.find(key);
+        if (it != map_.end())
+            return it->second;
+        RampFftTables t;
+        check_cuda(cudaMalloc(&t.spec, sizeof(double) * kRfN), "cudaMalloc(ramp spectrum)");
+        check_cuda(cudaMalloc(&t.tw, sizeof(double2) * kRfN), "cudaMalloc(ramp twiddles)");
+        ramp_fft_tables<<<kRfN / 128, 128, 0, st>>>(t.spec, t.tw, kRfN, tau);
+        check_cuda(cudaGetLastError(), "ramp_fft_tables");
+        check_cuda(cudaStreamSynchronize(st), "ramp_fft_tables");
+        ++g_launches;
+        return map_.emplace(key, t).first->second;
+    }
+
+  private:
+    std::mutex mu_;
+    std::map<std::tuple<int, double>, RampFftTables> map_;
+};
+
+inline bool ramp_fft_supported(int W) { return W >= 1 && W <= kRfMaxW; }
+
+// raw, out: count*H rows of W floats on the device (may alias).
+inline void ramp_fft_device(const float* raw, float* out, int W, int H, int count, double tau,
+                            cudaStream_t st) {
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    const RampFftTables t = RampFftCache::get().tables(dev, tau, st);
+    static bool attr_set[64] = {};
+    if (dev < 64 && !attr_set[dev]) {
+        check_cuda(cudaFuncSetAttribute(ramp_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kRfSmemBytes),
+                   "cudaFuncSetAttribute(ramp_fft_rows)");
+        attr_set[dev] = true;
+    }
+    const long long rows = (long long)H * count;
+    const long long pairs = (rows + 1) / 2;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long grid = std::min<long long>(pairs, (long long)nsm * 2); // 2 CTAs/SM
+    if (grid < 1)
+        return;
+    ramp_fft_rows<<<(unsigned)grid, kRfT, kRfSmemBytes, st>>>(raw, out, W, rows, t.spec, t.tw);
+    check_cuda(cudaGetLastError(), "ramp_fft_rows");
+    ++g_launches;
+}
+
+} // namespace cbb

@@ -13,12 +13,14 @@
 #pragma once
 
 #include <cmath>
+#include <cstdlib>
 #include <cufft.h>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 #include "../../include/conebeam_b200.h"
+#include "ramp_fft.cuh"
 
 namespace cbb {
 
@@ -135,9 +137,11 @@ class RampPlans {
 
 constexpr long long kRampRows = 8192; // rows per FFT call (~0.5 GB of float64 work space)
 
-// raw and out: count*H rows of W floats (device); may alias.
-inline void ramp_filter_device(const float* raw, float* out, int W, int H, int count, double tau,
-                               cudaStream_t st) {
+// raw and out: count*H rows of W floats (device); may alias. cuFFT path,
+// kept for detectors wider than the fused kernel's 2048 pixels (and as the
+// comparison baseline, CBB_RAMP_CUFFT=1).
+inline void ramp_filter_cufft(const float* raw, float* out, int W, int H, int count, double tau,
+                              cudaStream_t st) {
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const long long rows_total = (long long)H * count;
@@ -168,6 +172,21 @@ inline void ramp_filter_device(const float* raw, float* out, int W, int H, int c
         g_launches += 3;
     }
     check_cuda(cudaEventRecord(p.last, st), "ramp: record use");
+}
+
+} // namespace cbb
+
+namespace cbb {
+
+// The FDK filter stage: the fused shared-memory FFT kernel (ramp_fft.cuh)
+// when the detector fits its N = 4096 transform, else cuFFT.
+inline void ramp_filter_device(const float* raw, float* out, int W, int H, int count, double tau,
+                               cudaStream_t st) {
+    static const bool force_cufft = std::getenv("CBB_RAMP_CUFFT") != nullptr;
+    if (ramp_fft_supported(W) && !force_cufft)
+        ramp_fft_device(raw, out, W, H, count, tau, st);
+    else
+        ramp_filter_cufft(raw, out, W, H, count, tau, st);
 }
 
 } // namespace cbb

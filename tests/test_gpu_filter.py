@@ -51,6 +51,33 @@ def test_ramp_filter_matches_numpy(cuda):
     assert np.array_equal(t.cpu().numpy(), got)
 
 
+@pytest.mark.parametrize("width,rows", [(1248, 7), (1536, 6), (2048, 3), (2049, 3), (5, 9),
+                                        (1, 4)])
+def test_fused_fft_filter_widths_and_odd_row_counts(cuda, width, rows):
+    """The fused shared-memory FFT kernel (ramp_fft.cuh: row pairs as one
+    complex N = 4096 transform, W <= 2048) and the cuFFT path beyond it,
+    against numpy float64 at the BASELINE detector widths (1248, 1536), the
+    fused kernel's limit, an odd number of rows (last pair half empty) and
+    degenerate widths; in place as well."""
+    import torch
+
+    r = np.random.default_rng(width * 31 + rows)
+    raw = (r.standard_normal((1, rows, width)) * 50).astype(np.float32)
+    raw[0, 0, :] = 0.0
+    raw[0, -1, : min(width, 7)] = 1e3
+    tau = 0.2 if width % 2 == 0 else 0.32
+    ref = numpy_ramp(raw, tau)
+    t = torch.from_numpy(raw).cuda()
+    out = torch.empty_like(t)
+    pkg.ramp_filter_device(t, out, tau)
+    got = out.cpu().numpy()
+    scale = float(np.abs(ref).max())
+    assert np.abs(got - ref).max() <= 1e-6 * scale
+    assert np.mean(got == ref) > 0.99
+    pkg.ramp_filter_device(t, t, tau)
+    assert np.array_equal(t.cpu().numpy(), got)
+
+
 def test_compare_volumes_device_matches_numpy(cuda):
     """GPU volume metrics vs the reference harness definitions
     (proj/src/bench.cpp:65-102) computed in numpy float64."""
