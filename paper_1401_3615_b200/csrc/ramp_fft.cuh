@@ -21,8 +21,9 @@
 //     every thread holding exactly the 16 frequencies the inverse transform's
 //     first pass needs, so the spectrum multiply and that pass happen in
 //     registers; the inverse's last pass stores the W outputs (scaled by 1/N,
-//     folded into H) straight to global memory. Shared memory (re / im double
-//     planes, one pad word per 16) carries only the 4 remaining exchanges.
+//     folded into H) straight to global memory. Shared memory (one complex
+//     double plane, one pad element per 16) carries only the 4 remaining
+//     exchanges.
 //
 // FP64 (64 lanes/clk/SM on B200) bounds it: ~370k FP64 ops per row pair.
 // Detectors wider than 2048 pixels keep the cuFFT path.
@@ -44,9 +45,18 @@ extern thread_local uint64_t g_launches;
 constexpr int kRfN = 4096;                     // FFT length
 constexpr int kRfT = 256;                      // threads per FFT (N / 16)
 constexpr int kRfMaxW = 2048;                  // N >= 2W - 1
-__host__ __device__ constexpr int rf_pad(int i) { return i + (i >> 4); }
-constexpr int kRfPlane = rf_pad(kRfN);         // doubles per re / im plane
-constexpr int kRfSmemBytes = 2 * kRfPlane * 8; // 69632 B
+// XOR swizzle of the complex plane (16-byte elements, 8 per 128-byte bank
+// row): the stride-16 writes of the first pass, the stride-256 reads and the
+// Ns = 16 writes all hit 8 distinct bank groups per 8-lane phase, with no pad.
+__host__ __device__ constexpr int rf_sw(int i) { return i ^ ((i >> 4) & 7); }
+constexpr int kRfPlane = kRfN;                 // complex elements in the plane
+// complex plane, spectrum (N/2 + 1, padded to N/2 + 2), 272 twiddle bases,
+// then (STAGE) two stages of two prefetched rows of NZ * 256 floats
+constexpr int kRfFixedBytes = kRfPlane * 16 + (kRfN / 2 + 2) * 8 + 272 * 16; // 86288 B
+__host__ __device__ constexpr bool rf_stage(int nz) { return nz <= 6; }
+__host__ __device__ constexpr int rf_smem_bytes(int nz) {
+    return kRfFixedBytes + (rf_stage(nz) ? 2 * 2 * nz * kRfT * 4 : 0);
+}
 
 struct cd {
     double x, y;
@@ -102,11 +112,32 @@ __device__ __forceinline__ void w16(cd& v) {
 
 // 16-point DFT of v[0..15] (input in natural order). Output X[k] lands in
 // v[4 (k % 4) + k / 4] (radix-4 x radix-4, n = 4 n1 + n2, k = k1 + 4 k2).
-template <bool INV>
+// NZ: inputs v[NZ..15] are known to be zero (the zero-padded half of the
+// forward transform's first pass): step 1 skips them. QN: only outputs
+// X[0..QN) are needed (the inverse's last pass keeps the W < N samples):
+// step 3 computes only those.
+template <bool INV, int NZ = 16, int QN = 16>
 __device__ __forceinline__ void dft16(cd (&v)[16]) {
 #pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2)
-        dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]); // v[4 k1 + n2] = A[n2][k1]
+    for (int n2 = 0; n2 < 4; ++n2) {
+        const int nz = (NZ > n2) + (NZ > 4 + n2) + (NZ > 8 + n2) + (NZ > 12 + n2);
+        if (nz >= 3) {
+            dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]); // v[4 k1 + n2] = A[n2][k1]
+        } else if (nz == 2) { // (a, b, 0, 0): a + b, a -+ i b, a - b, a +- i b
+            const cd a = v[n2], b = v[4 + n2];
+            const cd ib = INV ? cd{-b.y, b.x} : cd{b.y, -b.x};
+            v[n2] = a + b;
+            v[4 + n2] = a + ib;
+            v[8 + n2] = a - b;
+            v[12 + n2] = a - ib;
+        } else if (nz == 1) { // (a, 0, 0, 0): a everywhere
+            v[4 + n2] = v[n2];
+            v[8 + n2] = v[n2];
+            v[12 + n2] = v[n2];
+        } else {
+            v[n2] = v[4 + n2] = v[8 + n2] = v[12 + n2] = cd{0.0, 0.0};
+        }
+    }
     w16<INV, 1>(v[5]);
     w16<INV, 2>(v[6]);
     w16<INV, 3>(v[7]);
@@ -117,28 +148,43 @@ __device__ __forceinline__ void dft16(cd (&v)[16]) {
     w16<INV, 6>(v[14]);
     w16<INV, 9>(v[15]);
 #pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1)
-        dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    for (int k1 = 0; k1 < 4; ++k1) {
+        // outputs k = k1 + 4 k2 for k2 = 0..3 (QN: only those < QN)
+        const int nk = (QN > k1) + (QN > 4 + k1) + (QN > 8 + k1) + (QN > 12 + k1);
+        if (nk >= 3) {
+            dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+        } else if (nk >= 1) {
+            const cd a0 = v[4 * k1], a1 = v[4 * k1 + 1], a2 = v[4 * k1 + 2], a3 = v[4 * k1 + 3];
+            const cd t0 = a0 + a2, t2 = a1 + a3;
+            v[4 * k1] = t0 + t2;
+            if (nk == 2) {
+                const cd t1 = a0 - a2, t3 = a1 - a3;
+                const cd rt3 = INV ? cd{-t3.y, t3.x} : cd{t3.y, -t3.x};
+                v[4 * k1 + 1] = t1 + rt3;
+            }
+        }
+    }
 }
 __device__ __forceinline__ constexpr int x16(int k) { return 4 * (k % 4) + k / 4; }
 
 // One Stockham pass over shared memory: read 16 points at stride 256,
-// twiddle by exp(-+2 pi i r (j % NS) / (16 NS)), DFT16, write at stride NS.
-template <bool INV, int NS, bool READ, bool WRITE>
-__device__ __forceinline__ void rf_pass(cd (&v)[16], double* re, double* im,
-                                        const double2* __restrict__ tw, int j) {
+// twiddle by w1^r (w1 = exp(-+2 pi i (j % NS) / (16 NS)), precomputed per
+// thread), DFT16, write at stride NS (or leave the outputs in registers in
+// natural order: v[q] = X[j + 256 q]).
+template <bool INV, int NS, bool READ, bool WRITE, int NZ = 16, int QN = 16>
+__device__ __forceinline__ void rf_pass(cd (&v)[16], double2* buf, const double2* tws, int j) {
     if (READ) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            const int i = rf_pad(j + r * kRfT);
-            v[r] = cd{re[i], im[i]};
+            const double2 x = buf[rf_sw(j + r * kRfT)];
+            v[r] = cd{x.x, x.y};
         }
         __syncthreads(); // every read done before this pass's writes
     }
     if (NS > 1) {
-        // w1 = exp(-2 pi i e / 4096), e = (j % NS) * 4096 / (16 NS); w_r = w1^r
-        const double2 t = __ldg(tw + (j % NS) * (kRfN / (16 * NS)));
-        const cd w1 = INV ? cd{t.x, -t.y} : cd{t.x, t.y};
+        // w1 = exp(-+2 pi i (j % NS) / (16 NS)) from the block's table
+        const double2 t = tws[NS == 16 ? (j % 16) : 16 + j];
+        const cd w1{t.x, INV ? -t.y : t.y};
         cd w = w1;
 #pragma unroll
         for (int r = 1; r < 16; ++r) {
@@ -147,18 +193,14 @@ __device__ __forceinline__ void rf_pass(cd (&v)[16], double* re, double* im,
                 w = cmul(w, w1);
         }
     }
-    dft16<INV>(v);
+    dft16<INV, NZ, QN>(v);
     if (WRITE) {
         const int base = (j / NS) * NS * 16 + (j % NS);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int i = rf_pad(base + q * NS);
-            re[i] = v[x16(q)].x;
-            im[i] = v[x16(q)].y;
-        }
+        for (int q = 0; q < 16; ++q)
+            buf[rf_sw(base + q * NS)] = make_double2(v[x16(q)].x, v[x16(q)].y);
         __syncthreads();
     } else {
-        // outputs in natural order for the caller: X[j + 256 q] = v[x16(q)]
         cd o[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q)
@@ -170,44 +212,92 @@ __device__ __forceinline__ void rf_pass(cd (&v)[16], double* re, double* im,
 }
 
 // rows: `rows` rows of W floats (row-major, row r at raw + r * W); pairs of
-// rows (2p, 2p+1) per iteration; grid-stride over pairs. spec: N real
-// spectrum values of h, scaled by 1/N. tw: exp(-2 pi i e / N), e < N.
+// rows (2p, 2p+1) per iteration; grid-stride over pairs. spec: the real
+// spectrum of h for k <= N/2 (it is even: H[N-k] = H[k]), scaled by 1/N.
+// tw: exp(-2 pi i e / N), e < N. NZ = ceil(W / 256): inputs j + 256 r with
+// r >= NZ are padding (and so are outputs with q >= NZ).
+template <int NZ>
 __global__ void __launch_bounds__(kRfT, 2)
 ramp_fft_rows(const float* raw, float* out, int W, long long rows,
               const double* __restrict__ spec, const double2* __restrict__ tw) {
-    extern __shared__ double rf_smem[];
-    double* re = rf_smem;
-    double* im = rf_smem + kRfPlane;
+    extern __shared__ double2 rf_smem[];
+    // complex plane (XOR-swizzled, see rf_sw)
+    double2* buf = rf_smem;
+    double* hs = reinterpret_cast<double*>(rf_smem + kRfPlane); // N/2 + 1 spectrum values
+    // twiddle bases of the two twiddled passes: [0, 16) for Ns = 16
+    // (exp(-2 pi i m / 256)), [16, 272) for Ns = 256 (exp(-2 pi i j / 4096))
+    double2* tws = reinterpret_cast<double2*>(hs + kRfN / 2 + 2);
+    // prefetch stages: rows of the next pair are copied while this one is
+    // transformed (cp.async, 4-byte granules: any W)
+    float* stg = reinterpret_cast<float*>(tws + 272);
+    constexpr bool STAGE = rf_stage(NZ);
+    constexpr int SROW = NZ * kRfT;
     const int j = threadIdx.x;
+    for (int k = j; k <= kRfN / 2; k += kRfT)
+        hs[k] = spec[k];
+    tws[16 + j] = __ldg(tw + j);
+    if (j < 16)
+        tws[j] = __ldg(tw + j * (kRfN / 256));
     const long long pairs = (rows + 1) / 2;
-    for (long long p = blockIdx.x; p < pairs; p += gridDim.x) {
+    auto prefetch = [&](long long p, int s) {
+        if (p < pairs) {
+            const float* r1 = raw + (2 * p) * (long long)W;
+            const int nrow = 2 * p + 1 < rows ? 2 : 1;
+            for (int e = j; e < nrow * W; e += kRfT) {
+                const int row = e >= W, n = e - row * W;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(stg + (2 * s + row) * SROW + n);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(r1 + e));
+            }
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    if (STAGE)
+        prefetch(blockIdx.x, 0);
+    __syncthreads();
+    int s = 0;
+    for (long long p = blockIdx.x; p < pairs; p += gridDim.x, s ^= 1) {
         const float* r1 = raw + (2 * p) * (long long)W;
         const bool two = 2 * p + 1 < rows;
         const float* r2 = r1 + W;
         cd v[16];
+        if (STAGE) {
+            prefetch(p + gridDim.x, s ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads(); // this pair's rows are in stage s for every thread
+            const float* a = stg + 2 * s * SROW;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int n = j + r * kRfT;
-            const bool in = n < W;
-            v[r] = cd{in ? (double)__ldg(r1 + n) : 0.0, (in && two) ? (double)__ldg(r2 + n) : 0.0};
+            for (int r = 0; r < 16; ++r) {
+                const int n = j + r * kRfT;
+                const bool in = r < NZ && n < W;
+                v[r] = cd{in ? (double)a[n] : 0.0, (in && two) ? (double)a[SROW + n] : 0.0};
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int n = j + r * kRfT;
+                const bool in = r < NZ && n < W;
+                v[r] = cd{in ? (double)__ldg(r1 + n) : 0.0,
+                          (in && two) ? (double)__ldg(r2 + n) : 0.0};
+            }
         }
         // forward: Ns = 1 (from registers), 16, 256 (ends in registers)
-        rf_pass<false, 1, false, true>(v, re, im, tw, j);
-        rf_pass<false, 16, true, true>(v, re, im, tw, j);
-        rf_pass<false, 256, true, false>(v, re, im, tw, j);
+        rf_pass<false, 1, false, true, NZ>(v, buf, tws, j);
+        rf_pass<false, 16, true, true>(v, buf, tws, j);
+        rf_pass<false, 256, true, false>(v, buf, tws, j);
         // spectrum multiply: thread j holds Z[j + 256 q] in v[q] -- exactly
         // the inverse's first-pass inputs (stride N/16 = 256)
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const double h = __ldg(spec + j + q * kRfT);
+            const int k = j + q * kRfT;
+            const double h = hs[k <= kRfN / 2 ? k : kRfN - k];
             v[q] = cd{v[q].x * h, v[q].y * h};
         }
-        rf_pass<true, 1, false, true>(v, re, im, tw, j);
-        rf_pass<true, 16, true, true>(v, re, im, tw, j);
-        rf_pass<true, 256, true, false>(v, re, im, tw, j);
+        rf_pass<true, 1, false, true>(v, buf, tws, j);
+        rf_pass<true, 16, true, true>(v, buf, tws, j);
+        rf_pass<true, 256, true, false, 16, NZ>(v, buf, tws, j);
         float* o1 = out + (2 * p) * (long long)W;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < NZ; ++q) {
             const int n = j + q * kRfT;
             if (n < W) {
                 o1[n] = (float)v[q].x;
@@ -270,6 +360,20 @@ class RampFftCache {
     std::map<std::tuple<int, double>, RampFftTables> map_;
 };
 
+template <int NZ>
+void launch_ramp_fft(int dev, unsigned grid, const float* raw, float* out, int W, long long rows,
+                     const RampFftTables& t, cudaStream_t st) {
+    static bool attr_set[64] = {};
+    if (dev < 64 && !attr_set[dev]) {
+        check_cuda(cudaFuncSetAttribute(ramp_fft_rows<NZ>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        rf_smem_bytes(NZ)),
+                   "cudaFuncSetAttribute(ramp_fft_rows)");
+        attr_set[dev] = true;
+    }
+    ramp_fft_rows<NZ><<<grid, kRfT, rf_smem_bytes(NZ), st>>>(raw, out, W, rows, t.spec, t.tw);
+}
+
 inline bool ramp_fft_supported(int W) { return W >= 1 && W <= kRfMaxW; }
 
 // raw, out: count*H rows of W floats on the device (may alias).
@@ -278,13 +382,6 @@ inline void ramp_fft_device(const float* raw, float* out, int W, int H, int coun
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
     const RampFftTables t = RampFftCache::get().tables(dev, tau, st);
-    static bool attr_set[64] = {};
-    if (dev < 64 && !attr_set[dev]) {
-        check_cuda(cudaFuncSetAttribute(ramp_fft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kRfSmemBytes),
-                   "cudaFuncSetAttribute(ramp_fft_rows)");
-        attr_set[dev] = true;
-    }
     const long long rows = (long long)H * count;
     const long long pairs = (rows + 1) / 2;
     int nsm = 148;
@@ -292,7 +389,13 @@ inline void ramp_fft_device(const float* raw, float* out, int W, int H, int coun
     const long long grid = std::min<long long>(pairs, (long long)nsm * 2); // 2 CTAs/SM
     if (grid < 1)
         return;
-    ramp_fft_rows<<<(unsigned)grid, kRfT, kRfSmemBytes, st>>>(raw, out, W, rows, t.spec, t.tw);
+    const int nz = (W + kRfT - 1) / kRfT;
+    if (nz <= 5)
+        launch_ramp_fft<5>(dev, (unsigned)grid, raw, out, W, rows, t, st);
+    else if (nz == 6)
+        launch_ramp_fft<6>(dev, (unsigned)grid, raw, out, W, rows, t, st);
+    else
+        launch_ramp_fft<8>(dev, (unsigned)grid, raw, out, W, rows, t, st);
     check_cuda(cudaGetLastError(), "ramp_fft_rows");
     ++g_launches;
 }

@@ -73,7 +73,11 @@ def test_fused_fft_filter_widths_and_odd_row_counts(cuda, width, rows):
     got = out.cpu().numpy()
     scale = float(np.abs(ref).max())
     assert np.abs(got - ref).max() <= 1e-6 * scale
-    assert np.mean(got == ref) > 0.99
+    # rows travel in pairs through one complex transform: a row of zeros
+    # picks up float64 round-off of its partner (~1e-16 of it), not exact 0
+    zero = ~raw.any(axis=-1)
+    assert np.abs(got[zero]).max(initial=0.0) <= 1e-12 * scale
+    assert np.mean(got[~zero] == ref[~zero]) > 0.99
     pkg.ramp_filter_device(t, t, tau)
     assert np.array_equal(t.cpu().numpy(), got)
 
