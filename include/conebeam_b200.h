@@ -257,6 +257,27 @@ cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometr
                                        const cbb_options* options, int32_t* err_flag,
                                        void* stream);
 
+/* ---- TMA-staged back-projection from raw projections (no packing) ---------
+ * cbb_scan_device: per projection of `count` (rows x width floats each,
+ * raw_stride floats apart), flags[p] = 1 when a pixel has |value| >= 2^86
+ * (the exact mode's fast division needs the flag) and bit 2
+ * of *err_flag on a non-finite pixel (ProjectionImage::validate). flags: count
+ * uint32 on the device. Enqueued on stream.
+ * cbb_backproject_raw_device: cbb_backproject_device on RAW projections:
+ * raw points at row band->raw_row0 (0 when band is NULL) of projection 0,
+ * raw_stride floats between projections; flags from cbb_scan_device. Each
+ * block's detector footprint is staged in shared memory by TMA. Same bits as
+ * the packed path. Falls back to packing internally when the footprint boxes
+ * do not fit (coarse voxels) or rows are not 16-byte aligned. */
+cbb_status cbb_scan_device(const float* raw, int64_t raw_stride, int32_t width, int32_t rows,
+                           int32_t count, uint32_t* flags, int32_t* err_flag, void* stream);
+cbb_status cbb_backproject_raw_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                      int32_t z_begin, int32_t z_end, const float* raw,
+                                      int64_t raw_stride, int32_t width, int32_t height,
+                                      const cbb_row_band* band, int32_t count, const double* mats,
+                                      const uint32_t* flags, const cbb_options* options,
+                                      int32_t* err_flag, void* stream);
+
 /* ProjectionImage::validate on the device (proj/src/dataset.cpp:123-129):
  * sets bit 2 of *err_flag if any of the n floats is not finite. For the
  * uploading rank of a row-band pipeline, whose own band skips rows. */

@@ -13,6 +13,9 @@ from .errors import InternalError, error_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libconebeam_b200.so")
+# experiments only: load another build of the same library (e.g. a kernel
+# variant compiled with different -D flags); the product default is LIB_PATH
+LIB_PATH = os.environ.get("CBB_LIB_PATH", LIB_PATH)
 
 # Every symbol declared in include/conebeam_b200.h (checked by tests).
 EXPORTS = (
@@ -26,6 +29,7 @@ EXPORTS = (
     "cbb_backproject_device_band", "cbb_check_finite_device", "cbb_reconstruct_images",
     "cbb_release_cached_memory", "cbb_ipc_alloc", "cbb_ipc_free", "cbb_ipc_open",
     "cbb_ipc_close", "cbb_stream_write_flag", "cbb_stream_wait_flag", "cbb_memcpy_h2d_async",
+    "cbb_scan_device", "cbb_backproject_raw_device",
 )
 
 
@@ -155,6 +159,14 @@ def _declare(L) -> None:
                                               _VP, _VP]
     L.cbb_check_finite_device.restype = C.c_int
     L.cbb_check_finite_device.argtypes = [_VP, C.c_int64, _VP, _VP]
+    L.cbb_scan_device.restype = C.c_int
+    L.cbb_scan_device.argtypes = [_VP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _VP, _VP,
+                                  _VP]
+    L.cbb_backproject_raw_device.restype = C.c_int
+    L.cbb_backproject_raw_device.argtypes = [_VP, C.POINTER(VolumeGeometryC), C.c_int32,
+                                             C.c_int32, _VP, C.c_int64, C.c_int32, C.c_int32,
+                                             C.POINTER(RowBandC), C.c_int32, _VP, _VP,
+                                             C.POINTER(OptionsC), _VP, _VP]
     for name, args in (("cbb_ipc_alloc", [C.c_int64, C.POINTER(_VP), _VP]),
                        ("cbb_ipc_free", [_VP]), ("cbb_ipc_open", [_VP, C.POINTER(_VP)]),
                        ("cbb_ipc_close", [_VP]),

@@ -400,6 +400,57 @@ def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: 
         C.byref(band.c()), C.byref(oc), err, C.c_void_p(s.cuda_stream)))
 
 
+def scan_device(raw, flags, err_flag=None, stream=None) -> None:
+    """cbb_scan_device: per-projection numerator-range flags (uint32 / int32
+    CUDA tensor of N entries) and the non-finite check (err_flag bit 2) of raw
+    projections (contiguous CUDA float32 (N, rows, W))."""
+    import torch
+
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
+        raise ValidationError("scan_device: raw must be a contiguous CUDA float32 (N, R, W) tensor")
+    n, rows, w = raw.shape
+    if flags.numel() * flags.element_size() < 4 * n:
+        raise ValidationError("scan_device: flags too small")
+    s = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    err = None if err_flag is None else err_flag.data_ptr()
+    _lib.check(_lib.lib().cbb_scan_device(raw.data_ptr(), rows * w, w, rows, n, flags.data_ptr(),
+                                          err, C.c_void_p(s.cuda_stream)))
+
+
+def backproject_raw_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: int, raw,
+                           width: int, height: int, count: int, matrices: np.ndarray, flags,
+                           options: Optional[Options] = None, err_flag=None, stream=None,
+                           first: int = 0, band: Optional[RowBand] = None) -> None:
+    """cbb_backproject_raw_device: back-projection straight from raw
+    projections (contiguous CUDA float32 (N, rows, W): the full detector, or
+    the band's rows with `band`), each block's footprint staged in shared
+    memory by TMA; `flags` from scan_device over the same projections.
+    Projections [first, first + count) of the tensor are used."""
+    import torch
+
+    if not (vol_slab.is_cuda and vol_slab.dtype == torch.float32 and vol_slab.is_contiguous()):
+        raise ValidationError("backproject_raw_device: vol_slab must be a contiguous CUDA float32 tensor")
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
+        raise ValidationError("backproject_raw_device: raw must be a contiguous CUDA float32 (N, R, W) tensor")
+    L = geometry.edge_voxels
+    if vol_slab.numel() < (z_end - z_begin) * L * L:
+        raise ValidationError("backproject_raw_device: slab tensor too small")
+    m = validate_matrices(matrices)
+    n, rows, w = raw.shape
+    if m.shape[0] < count or first + count > n or w != width:
+        raise ValidationError("backproject_raw_device: projection count or width mismatch")
+    oc, _keep = (options or Options()).to_c()
+    g = geometry_c(geometry)
+    s = stream if stream is not None else torch.cuda.current_stream(vol_slab.device)
+    err = None if err_flag is None else err_flag.data_ptr()
+    stride = rows * w
+    _lib.check(_lib.lib().cbb_backproject_raw_device(
+        vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end),
+        raw.data_ptr() + 4 * int(first) * stride, stride, int(width), int(height),
+        None if band is None else C.byref(band.c()), int(count), _ptr(m),
+        flags.data_ptr() + 4 * int(first), C.byref(oc), err, C.c_void_p(s.cuda_stream)))
+
+
 def ramp_filter_device(raw, out, pixel_mm: float, stream=None) -> None:
     """FDK row-wise Shepp-Logan ramp filter on the GPU (cbb_ramp_filter_device):
     raw, out: contiguous CUDA float32 tensors (N, H, W) (may be the same)."""

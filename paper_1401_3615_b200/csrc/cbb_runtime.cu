@@ -40,6 +40,7 @@
 
 #include "../../include/conebeam_b200.h"
 #include "bp_kernels.cuh"
+#include "bp_tma.cuh"
 #include "ramp_filter.cuh"
 #include "metrics.cuh"
 #include "texture_variant.cuh"
@@ -47,6 +48,7 @@
 #include "runtime_common.cuh"
 #include "ipc.cuh"
 #include "launch.cuh"
+#include "launch_tma.cuh"
 #include "memory.cuh"
 #include "pipeline.cuh"
 
@@ -477,6 +479,88 @@ cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometr
         const cbb_options opt = resolve_options(options);
         launch_backproject(vol_slab, *geometry, z_begin, z_end, packed, width, height, count,
                            mats, opt, err_flag, static_cast<cudaStream_t>(stream), 0, 0, &b);
+    });
+}
+
+cbb_status cbb_scan_device(const float* raw, int64_t raw_stride, int32_t width, int32_t rows,
+                           int32_t count, uint32_t* flags, int32_t* err_flag, void* stream) {
+    return guarded([&] {
+        if (!raw || !flags || count < 0 || width < 1 || rows < 0)
+            fail(CBB_ERR_INVALID, "cbb_scan_device: bad argument");
+        if (raw_stride < (int64_t)width * rows)
+            fail(CBB_ERR_INVALID, "cbb_scan_device: raw_stride below rows * width");
+        launch_scan(raw, width, rows, raw_stride, count, flags, err_flag,
+                    static_cast<cudaStream_t>(stream));
+    });
+}
+
+cbb_status cbb_backproject_raw_device(float* vol_slab, const cbb_volume_geometry* geometry,
+                                      int32_t z_begin, int32_t z_end, const float* raw,
+                                      int64_t raw_stride, int32_t width, int32_t height,
+                                      const cbb_row_band* band, int32_t count, const double* mats,
+                                      const uint32_t* flags, const cbb_options* options,
+                                      int32_t* err_flag, void* stream) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (!vol_slab || !raw || !mats || !flags)
+            fail(CBB_ERR_INVALID, "cbb_backproject_raw_device: null argument");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin > z_end)
+            fail(CBB_ERR_INVALID, "cbb_backproject_raw_device: bad slab [%d, %d)", z_begin, z_end);
+        validate_matrices(mats, count);
+        const RowBand b = band_from_c(band, height);
+        if (raw_stride < (int64_t)b.rn * width)
+            fail(CBB_ERR_INVALID, "cbb_backproject_raw_device: raw_stride below the band size");
+        if (band && z_end > z_begin && count > 0) {
+            const RowBand need =
+                row_band_for(*geometry, width, height, z_begin, z_end, mats, count);
+            if (need.rn > 0 && (need.r0 < b.r0 || need.r0 + need.rn > b.r0 + b.rn))
+                fail(CBB_ERR_INVALID,
+                     "cbb_backproject_raw_device: band rows [%d, %d) do not cover the slab's "
+                     "footprint [%d, %d)",
+                     b.r0, b.r0 + b.rn, need.r0, need.r0 + need.rn);
+        }
+        const cbb_options opt = resolve_options(options);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (count == 0 || z_end == z_begin)
+            return;
+        const TmaPlan plan = plan_tma(*geometry, width, height, z_begin, z_end, mats, count);
+        if (std::getenv("CBB_TRACE"))
+            std::fprintf(stderr, "cbb: tma plan ok %d pitch %d bh %d stages %d (need %d x %d)\n", plan.ok,
+                         plan.pitch, plan.bh, plan.stages, plan.bw_need, plan.bh_need);
+        if (plan.ok && tma_path_enabled() && (uintptr_t)raw % 16 == 0 && raw_stride % 4 == 0) {
+            launch_backproject_raw(vol_slab, *geometry, z_begin, z_end, raw, raw_stride, width,
+                                   height, b.r0, b.rn, count, mats, flags, plan, opt, err_flag,
+                                   st);
+            return;
+        }
+        // footprint too large for the staged boxes (coarse voxels), unaligned
+        // rows or CBB_BP_PATH=quad: pack into a scratch buffer, gather kernel
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        const int qp = quad_pitch_cells(width);
+        const RowBand pb = b.is_full(height) ? b : row_band_for(*geometry, width, height,
+                                                                z_begin, z_end, mats, count);
+        const size_t per = (size_t)qp * pb.qn * 16 + kMetaBytes;
+        const int step = std::min(count, std::max(opt.batch, (int)((size_t(2) << 30) / per)));
+        void* packed = DevicePool::get().alloc(dev, per * step);
+        try {
+            for (int c0 = 0; c0 < count; c0 += step) {
+                const int n = std::min(step, count - c0);
+                launch_pack_band(raw + (long long)c0 * raw_stride, b.r0, b.rn, raw_stride, width,
+                                 height, n, packed, pb, st, err_flag);
+                launch_backproject(vol_slab, *geometry, z_begin, z_end, packed, width, height, n,
+                                   mats + 12 * (size_t)c0, opt, err_flag, st, 0, 0, &pb);
+            }
+        } catch (...) {
+            cudaStreamSynchronize(st);
+            DevicePool::get().release(dev, packed);
+            throw;
+        }
+        // the pool hands the buffer out again only after this stream's work
+        // (released buffers are reused in stream order by the same caller)
+        CK(cudaStreamSynchronize(st));
+        DevicePool::get().release(dev, packed);
     });
 }
 
