@@ -269,6 +269,20 @@ cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometr
  * block's detector footprint is staged in shared memory by TMA. Same bits as
  * the packed path. Falls back to packing internally when the footprint boxes
  * do not fit (coarse voxels) or rows are not 16-byte aligned. */
+/* The staging plan cbb_backproject_raw_device and cbb_reconstruct (one GPU,
+ * whole stack known) use for a slab: staged = 1 when the TMA kernel runs
+ * (box_width x box_rows floats per block and projection, `stages` deep),
+ * 0 when the footprint boxes exceed the shared-memory budget (coarse voxels),
+ * rows are not 16-byte aligned (width % 4 != 0) or CBB_BP_PATH=quad: then the
+ * packed-quad kernel runs. Host-only (no GPU needed). */
+typedef struct cbb_tma_plan_info {
+    int32_t staged;
+    int32_t box_width, box_rows, stages;
+    int32_t footprint_width, footprint_rows; /* sampled bound incl. margins */
+} cbb_tma_plan_info;
+cbb_status cbb_tma_plan(const cbb_volume_geometry* geometry, int32_t width, int32_t height,
+                        int32_t z_begin, int32_t z_end, const double* mats, int32_t count,
+                        cbb_tma_plan_info* out);
 cbb_status cbb_scan_device(const float* raw, int64_t raw_stride, int32_t width, int32_t rows,
                            int32_t count, uint32_t* flags, int32_t* err_flag, void* stream);
 cbb_status cbb_backproject_raw_device(float* vol_slab, const cbb_volume_geometry* geometry,

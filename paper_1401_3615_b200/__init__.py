@@ -8,7 +8,7 @@ from .backproject import (MODE_EXACT, MODE_FAST, Options, RowBand, Session, back
                           compare_volumes_device,
                           device_count, launch_count, pack_device, pack_device_band,
                           packed_layout, ramp_filter_device, reconstruct, reconstruct_arrays,
-                          backproject_raw_device, scan_device,
+                          backproject_raw_device, scan_device, tma_plan,
                           reconstruct_file, reconstruct_images, release_cached_memory,
                           row_band_for_slab,
                           stack_file_info)
@@ -22,7 +22,7 @@ __all__ = [
     "MODE_EXACT", "MODE_FAST", "Options", "RowBand", "Session", "backproject",
     "backproject_device", "backproject_texture_device", "check_finite_device", "compare_volumes_device",
     "pack_device_band", "release_cached_memory", "row_band_for_slab",
-    "backproject_raw_device", "scan_device",
+    "backproject_raw_device", "scan_device", "tma_plan",
     "device_count", "launch_count", "pack_device", "packed_layout", "ramp_filter_device", "reconstruct",
     "reconstruct_arrays", "reconstruct_file", "reconstruct_images", "stack_file_info", "ProjectionStack", "Volume", "read_stack", "read_volume",
     "write_stack", "write_volume", "ConebeamError", "FormatError", "GeometryError",

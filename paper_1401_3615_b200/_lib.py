@@ -29,7 +29,7 @@ EXPORTS = (
     "cbb_backproject_device_band", "cbb_check_finite_device", "cbb_reconstruct_images",
     "cbb_release_cached_memory", "cbb_ipc_alloc", "cbb_ipc_free", "cbb_ipc_open",
     "cbb_ipc_close", "cbb_stream_write_flag", "cbb_stream_wait_flag", "cbb_memcpy_h2d_async",
-    "cbb_scan_device", "cbb_backproject_raw_device",
+    "cbb_scan_device", "cbb_backproject_raw_device", "cbb_tma_plan",
 )
 
 
@@ -54,6 +54,12 @@ class OptionsC(C.Structure):
                 ("volume_is_zero", C.c_int32), ("slab_begin", C.c_int32),
                 ("slab_end", C.c_int32), ("ramp_filter", C.c_int32),
                 ("filter_pixel_mm", C.c_double), ("count_culled", C.c_int32)]
+
+
+class TmaPlanC(C.Structure):
+    _fields_ = [("staged", C.c_int32), ("box_width", C.c_int32), ("box_rows", C.c_int32),
+                ("stages", C.c_int32), ("footprint_width", C.c_int32),
+                ("footprint_rows", C.c_int32)]
 
 
 class RunStatsC(C.Structure):
@@ -159,6 +165,9 @@ def _declare(L) -> None:
                                               _VP, _VP]
     L.cbb_check_finite_device.restype = C.c_int
     L.cbb_check_finite_device.argtypes = [_VP, C.c_int64, _VP, _VP]
+    L.cbb_tma_plan.restype = C.c_int
+    L.cbb_tma_plan.argtypes = [C.POINTER(VolumeGeometryC), C.c_int32, C.c_int32, C.c_int32,
+                               C.c_int32, _VP, C.c_int32, C.POINTER(TmaPlanC)]
     L.cbb_scan_device.restype = C.c_int
     L.cbb_scan_device.argtypes = [_VP, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _VP, _VP,
                                   _VP]

@@ -400,6 +400,18 @@ def backproject_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: 
         C.byref(band.c()), C.byref(oc), err, C.c_void_p(s.cuda_stream)))
 
 
+def tma_plan(geometry: VolumeGeometry, width: int, height: int, z_begin: int, z_end: int,
+             matrices: np.ndarray) -> dict:
+    """cbb_tma_plan: whether the TMA-staged kernel runs for this slab and
+    stack (one GPU), with its box size and ring depth. Host-only."""
+    m = validate_matrices(matrices)
+    out = _lib.TmaPlanC()
+    _lib.check(_lib.lib().cbb_tma_plan(C.byref(geometry_c(geometry)), int(width), int(height),
+                                       int(z_begin), int(z_end), _ptr(m), m.shape[0],
+                                       C.byref(out)))
+    return {k: int(getattr(out, k)) for k, _ in out._fields_}
+
+
 def scan_device(raw, flags, err_flag=None, stream=None) -> None:
     """cbb_scan_device: per-projection numerator-range flags (uint32 / int32
     CUDA tensor of N entries) and the non-finite check (err_flag bit 2) of raw

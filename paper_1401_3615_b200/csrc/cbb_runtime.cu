@@ -482,6 +482,27 @@ cbb_status cbb_backproject_device_band(float* vol_slab, const cbb_volume_geometr
     });
 }
 
+cbb_status cbb_tma_plan(const cbb_volume_geometry* geometry, int32_t width, int32_t height,
+                        int32_t z_begin, int32_t z_end, const double* mats, int32_t count,
+                        cbb_tma_plan_info* out) {
+    return guarded([&] {
+        validate_geometry(geometry);
+        validate_detector(width, height);
+        if (!mats || !out || count < 1)
+            fail(CBB_ERR_INVALID, "cbb_tma_plan: null argument or count < 1");
+        if (z_begin < 0 || z_end > geometry->edge_voxels || z_begin >= z_end)
+            fail(CBB_ERR_INVALID, "cbb_tma_plan: bad slab [%d, %d)", z_begin, z_end);
+        validate_matrices(mats, count);
+        const TmaPlan p = plan_tma(*geometry, width, height, z_begin, z_end, mats, count);
+        out->staged = p.ok && tma_path_enabled() ? 1 : 0;
+        out->box_width = p.pitch;
+        out->box_rows = p.bh;
+        out->stages = p.stages;
+        out->footprint_width = p.bw_need;
+        out->footprint_rows = p.bh_need;
+    });
+}
+
 cbb_status cbb_scan_device(const float* raw, int64_t raw_stride, int32_t width, int32_t rows,
                            int32_t count, uint32_t* flags, int32_t* err_flag, void* stream) {
     return guarded([&] {

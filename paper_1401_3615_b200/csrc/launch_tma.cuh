@@ -88,6 +88,8 @@ inline TmaPlan plan_tma(const cbb_volume_geometry& g, int W, int H, int z_begin,
     mix(&g.voxel_mm, 8);
     mix(&g.origin_mm, 8);
     mix(mats, sizeof(double) * 12 * (size_t)count);
+    if (const char* e = std::getenv("CBB_TMA_BOX"))
+        mix(e, std::strlen(e));
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(h);
@@ -140,6 +142,13 @@ inline TmaPlan plan_tma(const cbb_volume_geometry& g, int W, int H, int z_begin,
                     bhh = std::max(bhh, std::floor(hy) + 2.0 - std::floor(ly) + 1.0);
                 }
     }
+    if (const char* e = std::getenv("CBB_TMA_BOX")) { // tests: force a box, blocks overflow
+        int fw = 0, fh = 0;
+        if (std::sscanf(e, "%dx%d", &fw, &fh) == 2 && fw > 0 && fh > 0) {
+            bw = fw - 2;
+            bhh = fh - 2;
+        }
+    }
     if (finite && bw > 0.0) {
         plan.bw_need = (int)bw + 2;
         plan.bh_need = (int)bhh + 2;
@@ -160,12 +169,11 @@ inline TmaPlan plan_tma(const cbb_volume_geometry& g, int W, int H, int z_begin,
     return plan;
 }
 
+// CBB_BP_PATH=quad selects the packed-quad gather kernel everywhere (read on
+// every call: tests switch it inside one process).
 inline bool tma_path_enabled() {
-    static const bool off = [] {
-        const char* e = std::getenv("CBB_BP_PATH");
-        return e && std::string(e) == "quad";
-    }();
-    return !off;
+    const char* e = std::getenv("CBB_BP_PATH");
+    return !(e && std::string(e) == "quad");
 }
 
 // Scans `count` raw projections (rows x W floats each, `stride` floats apart)

@@ -51,6 +51,10 @@ struct Worker {
     cudaEvent_t xfer_ev[2] = {};       // ChunkedXfer chunk events (copy stream)
     unsigned long long* d_counters = nullptr; // kCounterSlots culled-update counters
     bool count_culled = false;
+    // raw mode (TMA kernel, bp_tma.cuh): per-projection scan flags of the
+    // current batch, or of every resident projection
+    unsigned* d_flags = nullptr;
+    unsigned* d_flags_all = nullptr;
 
     ~Worker() {
         if (!copy)
@@ -78,6 +82,8 @@ struct Worker {
         pool.release(device, d_err);
         pool.release(device, d_counters);
         pool.release(device, d_packed_all);
+        pool.release(device, d_flags);
+        pool.release(device, d_flags_all);
         if (head_done)
             cudaEventDestroy(head_done);
         if (tail_done)
@@ -105,11 +111,11 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 // a fixed overhead), sampled on a 12 x 12 grid at the group's centre plane for
 // up to 4 of the n projections.
 std::vector<double> group_work(const cbb_volume_geometry& g, int W, int H, int z0, int z1,
-                               const double* mats, int n) {
+                               const double* mats, int n, int group = 8) {
     const int L = g.edge_voxels, S = 12, NP = std::min(n, 4);
     std::vector<double> gw;
-    for (int z = z0; z < z1; z += 8) {
-        const int pz = std::min(8, z1 - z);
+    for (int z = z0; z < z1; z += group) {
+        const int pz = std::min(group, z1 - z);
         const double zc = g.origin_mm + (z + (pz - 1) * 0.5) * g.voxel_mm;
         int on = 0;
         for (int k = 0; k < NP; ++k) {
@@ -176,6 +182,14 @@ struct Pipeline {
     std::vector<double> all_mats;  // resident mode: every matrix, for the tail pass
     const double* est_mats = nullptr; // matrices for choose_tails (else the first batch)
     int est_n = 0;
+    // Raw mode: one device, whole stack known, detector rows 16-byte aligned
+    // and footprint boxes within the shared-memory budget: the batches are
+    // scanned (scan_projections) and back-projected straight from the raw
+    // projections by the TMA-staged kernel -- no packing, and resident mode
+    // keeps the raw stack (4.8x smaller than the packed one).
+    bool raw_mode = false;
+    TmaPlan plan;
+    int tail_group() const { return raw_mode ? kTR : 8; }
 
     // Resident mode for a stack of known size: when every packed projection
     // fits in device memory (with 2 GB to spare), keep them all so a dense
@@ -235,9 +249,11 @@ struct Pipeline {
         if (const char* e = std::getenv("CBB_TAIL_FRAC"))
             frac = std::atof(e);
         for (auto& w : workers) {
-            const std::vector<double> gw = group_work(g, W, H, w->z_begin, w->z_end, mats, n);
+            const int gs = tail_group(); // head launches skip the tail: aligned to their z-blocks
+            const std::vector<double> gw =
+                group_work(g, W, H, w->z_begin, w->z_end, mats, n, gs);
             std::vector<int> gz;
-            for (int z = w->z_begin; z < w->z_end; z += 8)
+            for (int z = w->z_begin; z < w->z_end; z += gs)
                 gz.push_back(z);
             gz.push_back(w->z_end);
             const int G = (int)gw.size();
@@ -391,7 +407,53 @@ struct Pipeline {
     // to every worker. The caller guarantees src stays valid until the
     // upload completes (wait_stage for the staging ring).
     // stage >= 0: src is host staging slot `stage` (its reuse waits for this H2D).
+    // issue() in raw mode (one worker): upload (into the resident raw stack
+    // or a ring slot), optional ramp filter, scan, TMA back-projection.
+    void issue_raw(const float* src, const double* mats, int n, int stage) {
+        NvtxRange range("cbb batch (raw)");
+        Worker& w = *workers[0];
+        CK(cudaSetDevice(w.device));
+        const size_t bytes = raw_bytes_per_proj * n;
+        float* dst;
+        unsigned* flags;
+        if (resident) {
+            dst = static_cast<float*>(w.d_packed_all) + (size_t)submitted * W * H;
+            flags = w.d_flags_all + submitted;
+        } else {
+            dst = w.d_raw[slot];
+            flags = w.d_flags;
+            CK(cudaStreamWaitEvent(w.copy, w.raw_free[slot], 0));
+        }
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, w.copy));
+        CK(cudaEventRecord(w.h2d_done[slot], w.copy));
+        if (stage >= 0) {
+            CK(cudaEventRecord(w.stage_read[stage], w.copy));
+            stage_owner[stage] = 0;
+        }
+        CK(cudaStreamWaitEvent(w.compute, w.h2d_done[slot], 0));
+        start_timing(w);
+        if (opt.ramp_filter)
+            ramp_filter_device(dst, dst, W, H, n, opt.filter_pixel_mm, w.compute);
+        launch_scan(dst, W, H, (long long)W * H, n, flags, w.d_err, w.compute);
+        if (resident && submitted == 0)
+            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
+        w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, dst,
+                                           (long long)W * H, W, H, 0, H, n, mats, flags, plan, opt,
+                                           w.d_err, w.compute, resident ? w.tail_lo : 0,
+                                           resident ? w.tail_hi : 0,
+                                           w.count_culled ? w.d_counters : nullptr);
+        if (!resident)
+            CK(cudaEventRecord(w.raw_free[slot], w.compute));
+        ++nbatch;
+        if (resident)
+            std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
+        submitted += n;
+        slot = (slot + 1) % nslots;
+    }
+
     void issue(const float* src, const double* mats, int n, int stage = -1) {
+        if (raw_mode)
+            return issue_raw(src, mats, n, stage);
         NvtxRange range("cbb batch");
         const size_t bytes = raw_bytes_per_proj * n;
         // Batch k is uploaded once, by the root worker k mod G. Each other
@@ -609,7 +671,27 @@ struct Pipeline {
         NvtxRange range("cbb setup (bands, resident)");
         const auto t0 = std::chrono::steady_clock::now();
         set_bands(mats, count);
+        if (workers.size() == 1 && tma_path_enabled()) {
+            Worker& w = *workers[0];
+            plan = plan_tma(g, W, H, w.z_begin, w.z_end, mats, count);
+            raw_mode = plan.ok;
+            if (raw_mode) {
+                w.band = RowBand::full(H);
+                w.pk_bytes = raw_bytes_per_proj; // resident stack: raw projections
+                CK(cudaSetDevice(w.device));
+                w.d_flags = static_cast<unsigned*>(
+                    DevicePool::get().alloc(w.device, sizeof(unsigned) * opt.batch));
+            }
+            if (std::getenv("CBB_TRACE"))
+                std::fprintf(stderr, "cbb: raw mode %d (tma pitch %d bh %d stages %d)\n",
+                             (int)raw_mode, plan.pitch, plan.bh, plan.stages);
+        }
         enable_resident(count);
+        if (raw_mode && resident) {
+            Worker& w = *workers[0];
+            w.d_flags_all = static_cast<unsigned*>(
+                DevicePool::get().alloc(w.device, sizeof(unsigned) * count));
+        }
         if (std::getenv("CBB_TRACE"))
             std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
                          std::chrono::duration<double, std::milli>(
@@ -852,7 +934,14 @@ struct Pipeline {
             const int mid = tail_mid(*w);
             for (const auto& part : {std::make_pair(w->tail_lo, mid),
                                      std::make_pair(mid, w->tail_hi)}) {
-                if (part.second > part.first)
+                if (part.second > part.first && raw_mode)
+                    w->guarded += launch_backproject_raw(
+                        w->d_vol + plane * (part.first - w->z_begin), g, part.first,
+                        part.second, static_cast<const float*>(w->d_packed_all),
+                        (long long)W * H, W, H, 0, H, resident_count, all_mats.data(),
+                        w->d_flags_all, plan, opt, w->d_err, w->compute, 0, 0,
+                        w->count_culled ? w->d_counters : nullptr);
+                else if (part.second > part.first)
                     w->guarded += launch_backproject(
                         w->d_vol + plane * (part.first - w->z_begin), g, part.first,
                         part.second, w->d_packed_all, W, H, resident_count, all_mats.data(), opt,

@@ -357,3 +357,25 @@ def test_array_entry_points_check_sizes_before_the_library():
         pkg.reconstruct_images(np.zeros(7, np.float32), g, list(imgs), mats)
     with pytest.raises(pkg.ValidationError, match="differ in length"):
         pkg.reconstruct_images(np.zeros((8, 8, 8), np.float32), g, list(imgs), mats[:1])
+
+
+def test_tma_plan_for_baseline_configs(monkeypatch):
+    """Host-side staging plan of the TMA kernel (cbb_tma_plan, no GPU): the
+    0.5 / 0.25 mm configs (2, 3, 4) stage their footprint boxes in shared
+    memory; the coarse 2 mm / 1 mm volumes (configs 0, 1: boxes over the
+    budget), detectors whose rows are not 16-byte aligned and
+    CBB_BP_PATH=quad take the packed-quad kernel."""
+    for cid, staged in ((0, 0), (1, 0), (2, 1), (3, 1), (4, 1)):
+        cfg = synth.CONFIGS[cid]
+        m = synth.perturbed_matrices(cfg)
+        g = cfg.geometry
+        p = pkg.tma_plan(g, cfg.width, cfg.height, 0, g.edge_voxels, m)
+        assert p["staged"] == staged, (cid, p)
+        if staged:
+            assert p["box_width"] >= p["footprint_width"] and p["box_width"] % 16 == 0
+            assert p["box_rows"] >= p["footprint_rows"] and 3 <= p["stages"] <= 8
+    cfg = synth.CONFIGS[2]
+    m = synth.perturbed_matrices(cfg)
+    assert pkg.tma_plan(cfg.geometry, 1247, 960, 0, 512, m)["staged"] == 0
+    monkeypatch.setenv("CBB_BP_PATH", "quad")
+    assert pkg.tma_plan(cfg.geometry, 1248, 960, 0, 512, m)["staged"] == 0
