@@ -8,12 +8,14 @@ Workload (N=1): BASELINE config 2 -- 512^3 float32 volume at 0.5 mm, 496
 filtered projections of 1248x960 (seeded synthetic stand-in for RabbitCT,
 see paper_1401_3615_b200/synth.py), full-basis voxel updates L^3 * N.
 
-One step = one full reconstruction: zero the volume, pack the 496 resident
-projections into the gather layout, back-project them in batches of 32.
+One step = one full reconstruction: zero the volume, prepare the 496 resident
+projections, back-project them in batches of 32.
   value : inputs resident in HBM; device-timed with CUDA events; max over ranks.
   e2e   : the public host API (cbb_reconstruct through reconstruct_arrays) from
           pinned host projections to the host volume, H2D + kernels + D2H.
-Inputs (2.4 GB raw + 11.3 GB packed) exceed the 126 MB L2, so no flush is needed.
+Inputs (2.4 GB of raw projections) exceed the 126 MB L2, so no flush is needed.
+Prepare = scan_projections (flags, non-finite check) for the TMA-staged raw
+kernel (configs 2-4), or pack_quads for the gather kernel (coarse voxels).
 Multi-GPU (torchrun): each rank owns a z-slab of the same volume (strong
 scaling); no data-path collective in `value`.
 """
@@ -49,6 +51,8 @@ def parse():
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quad", action="store_true",
+                    help="packed-quad kernel even where the TMA-staged kernel applies")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the other-mode and 1024^3 secondary measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -248,6 +252,62 @@ def run_reference_arm(args):
 # our arm
 # ---------------------------------------------------------------------------------
 
+class SlabStep:
+    """One slab's device-resident step: zero the slab, prepare the
+    projections, back-project them. Prepare = scan_projections + the
+    TMA-staged raw kernel when cbb_tma_plan stages this slab's footprints
+    (configs 2-4), else pack_quads + the packed-quad gather kernel (coarse
+    voxels: configs 0-1). A worker whose slab projects onto a row band keeps
+    only those raw rows (copied once, untimed) or packs only those cell rows."""
+
+    def __init__(self, pkg, torch, dev, g, imgs, mats, z0, z1, opt, err, stream,
+                 packed=None, force_quad=False):
+        self.pkg, self.torch, self.g, self.mats, self.opt = pkg, torch, g, mats, opt
+        self.z0, self.z1, self.err, self.stream = z0, z1, err, stream
+        n, H, W = imgs.shape
+        self.n, self.H, self.W = n, H, W
+        L = g.edge_voxels
+        self.band = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
+        plan = pkg.tma_plan(g, W, H, z0, z1, mats)
+        self.staged = bool(plan["staged"]) and not force_quad
+        self.plan = plan
+        self.vol = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+        if self.staged:
+            self.kernel = "bp_tma_kernel"
+            full = self.band.raw_rows == H and self.band.raw_row0 == 0
+            self.src = imgs if full else imgs[:, self.band.raw_row0:
+                                              self.band.raw_row0 + self.band.raw_rows].contiguous()
+            self.src_band = None if full else self.band
+            self.flags = torch.zeros(n, dtype=torch.int32, device=dev)
+            self.proj_bytes = self.src[0].numel() * 4
+        else:
+            self.kernel = "bp_kernel"
+            self.imgs = imgs
+            self.packed = packed if packed is not None else torch.empty(
+                n * pkg.packed_layout(W, H)[2], dtype=torch.uint8, device=dev)
+            self.proj_bytes = self.band.packed_bytes(W, H)
+
+    def prep(self):
+        if self.staged:
+            self.pkg.scan_device(self.src, self.flags, self.err, self.stream)
+        else:
+            self.pkg.pack_device_band(self.imgs, self.band, self.packed, self.err, self.stream)
+
+    def backproject(self, vol=None):
+        vol = self.vol if vol is None else vol
+        if self.staged:
+            self.pkg.backproject_raw_device(vol, self.g, self.z0, self.z1, self.src, self.W,
+                                            self.H, self.n, self.mats, self.flags, self.opt,
+                                            self.err, self.stream, band=self.src_band)
+        else:
+            self.pkg.backproject_device(vol, self.g, self.z0, self.z1, self.packed, self.W,
+                                        self.H, self.n, self.mats, self.opt, self.err,
+                                        self.stream, band=self.band)
+
+    def release(self):
+        self.vol = self.src = self.packed = self.flags = None
+
+
 def calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world, args,
                     rebalance_slabs, rounds=2):
     """Times this rank's pack + back-projection step on its slab (untimed
@@ -255,10 +315,6 @@ def calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world, arg
     (rebalance_slabs) while max/mean > 1.02, at most `rounds` times."""
     import torch
 
-    n, H, W = imgs.shape
-    L = g.edge_voxels
-    nb_full = pkg.packed_layout(W, H)[2]
-    packed = torch.empty(n * nb_full, dtype=torch.uint8, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     opt = pkg.Options(batch=args.batch, mode=pkg.MODE_EXACT if args.mode == "exact"
                       else pkg.MODE_FAST)
@@ -266,15 +322,15 @@ def calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world, arg
     history = []
     for it in range(rounds + 1):
         z0, z1 = slabs[rank]
-        band = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
-        vol = torch.zeros(((z1 - z0), L, L), dtype=torch.float32, device=dev)
+        st = SlabStep(pkg, torch, dev, g, imgs, mats, z0, z1, opt, err, stream,
+                      force_quad=args.quad)
+        st.vol.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for rep in range(2):
             if rep == 1:
                 a.record(stream)
-            pkg.pack_device_band(imgs, band, packed, err, stream)
-            pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream,
-                                   band=band)
+            st.prep()
+            st.backproject()
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
@@ -283,11 +339,10 @@ def calibrate_slabs(pkg, dist, dev, g, imgs, mats, work, slabs, rank, world, arg
         times = [float(x.item()) for x in allt]
         imb = max(times) / (sum(times) / world)
         history.append(round(imb, 4))
-        del vol
+        st.release()
         if imb < 1.02 or it == rounds:
             break
         slabs = rebalance_slabs(work, slabs, times)
-    del packed
     torch.cuda.empty_cache()
     return {"slabs": [list(s) for s in slabs], "imbalance": history, "rounds": len(history) - 1}
 
@@ -338,14 +393,14 @@ def run_ours(args):
     else:
         slabs = [(0, L)]
     z0, z1 = slabs[rank]
-    # this rank packs only the detector rows its slab projects onto (the
-    # whole detector for a single 512^3 slab)
-    band = pkg.row_band_for_slab(g, W, H, z0, z1, mats)
-    nb = band.packed_bytes(W, H)
-    packed = torch.empty(n * pkg.packed_layout(W, H)[2], dtype=torch.uint8, device=dev)
-    vol = torch.empty(((z1 - z0), L, L), dtype=torch.float32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    # this rank's slab: TMA-staged raw path (scan + bp_tma_kernel) when the
+    # footprint boxes fit, else pack + gather; a band of rows when the slab
+    # projects onto one
+    sstep = SlabStep(pkg, torch, dev, g, imgs, mats, z0, z1, opt, err, stream,
+                     force_quad=args.quad)
+    band, nb, vol = sstep.band, sstep.proj_bytes, sstep.vol
 
     nbatch = (n + args.batch - 1) // args.batch
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -355,11 +410,10 @@ def run_ours(args):
         vol.zero_()
         if i is not None:
             ev[i][0].record(stream)
-        pkg.pack_device_band(imgs, band, packed, err, stream)
+        sstep.prep()
         if i is not None:
             ev[i][1].record(stream)
-        pkg.backproject_device(vol, g, z0, z1, packed, W, H, n, mats, opt, err, stream,
-                               band=band)
+        sstep.backproject()
         if i is not None:
             ev[i][2].record(stream)
 
@@ -400,7 +454,7 @@ def run_ours(args):
     c = SimpleNamespace(pkg=pkg, torch=torch, dist=dist, dev=dev, rank=rank, world=world,
                         local=local, args=args, cfg=cfg, mode=mode, g=g, mats=mats, imgs=imgs,
                         L=L, n=n, H=H, W=W, slabs=slabs, z0=z0, z1=z1, band=band, nb=nb,
-                        packed=packed, vol=vol, err=err, stream=stream,
+                        sstep=sstep, vol=vol, err=err, stream=stream,
                         total_updates=total_updates)
     roofline = roofline_entry(c, bp_ms, nbatch, clocks)
     line = {
@@ -416,9 +470,13 @@ def run_ours(args):
                        k: balance[k] for k in ("imbalance", "rounds")},
                    "row_band": {"rows": [band.raw_row0, band.raw_row0 + band.raw_rows],
                                 "cell_rows": band.cell_rows},
-                   "l2": (f"inputs larger than L2 ({imgs.numel() * 4 / 1e9:.1f} GB raw + "
-                          f"{n * nb / 1e9:.1f} GB packed vs 0.126 GB L2), no flush")},
-        "pack_ms_per_step": round(statistics.mean(pack_ms), 4),
+                   "l2": (f"inputs larger than L2 ({imgs.numel() * 4 / 1e9:.1f} GB of "
+                          f"projections, {n * nb / 1e9:.1f} GB read by the kernel per step, "
+                          f"vs 0.126 GB L2), no flush")},
+        "path": (f"TMA-staged raw projections (scan_projections + bp_tma_kernel, box "
+                 f"{sstep.plan['box_width']}x{sstep.plan['box_rows']} x {sstep.plan['stages']} "
+                 f"stages)" if sstep.staged else "packed quads (pack_quads + bp_kernel)"),
+        "prep_ms_per_step": round(statistics.mean(pack_ms), 4),
         "backproject_ms_per_step": round(statistics.mean(bp_ms), 4),
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -428,8 +486,8 @@ def run_ours(args):
     if not args.no_secondary:
         line["secondary"] = secondary_entries(c)
     if not args.no_e2e:
-        c.packed = None
-        del packed
+        sstep.packed = None
+        torch.cuda.empty_cache()
         line.update(e2e_entries(c))
         if line.get("culled_fraction") is not None and line["culled_fraction"] >= 0:
             # the same fraction counted only over the updates the kernel
@@ -471,15 +529,18 @@ def roofline_entry(c, bp_ms, nbatch, clocks):
     fp32_peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lane-ops/s (Tops) at max clock
     achieved = updates_per_launch * OPS_PER_UPDATE / (bp_launch_ms * 1e-3) / 1e12
     sm_load = clocks.get("sm_mhz") or sm_max
-    hbm_bytes = 8 * (z1 - z0) * L * L + proj_per_launch * nb  # volume rmw + packed inputs
+    # volume read-modify-write + the launch's inputs (raw rows for the staged
+    # kernel, packed cells for the gather kernel)
+    hbm_bytes = 8 * (z1 - z0) * L * L + proj_per_launch * nb
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        rec = json.load(open(tpath)).get(f"{cfg.name}/{args.mode}")
+        rec = json.load(open(tpath)).get(f"{cfg.name}/{args.mode}/{c.sstep.kernel}")
         if rec and c.world == 1:
             traffic = rec["dram_bytes_per_launch"]
             traffic_src = f"profiles/{rec['source']} (ncu --set full, one launch)"
     roofline = {
+        "kernel": c.sstep.kernel,
         "bound": "fp32", "achieved": round(achieved, 3), "peak": round(fp32_peak, 3),
         "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": traffic,
         "traffic_source": traffic_src, "algorithmic_bytes_per_launch": int(hbm_bytes),
@@ -506,23 +567,22 @@ def secondary_entries(c):
     config 3 (configs 0-3 share the scan) and the texture side number."""
     pkg, torch, dist, dev, args, cfg = c.pkg, c.torch, c.dist, c.dev, c.args, c.cfg
     g, mats, imgs, L, n, H, W = c.g, c.mats, c.imgs, c.L, c.n, c.H, c.W
-    z0, z1, packed, vol, err, stream, mode = c.z0, c.z1, c.packed, c.vol, c.err, c.stream, c.mode
+    z0, z1, vol, err, stream, mode = c.z0, c.z1, c.vol, c.err, c.stream, c.mode
     rank, world = c.rank, c.world
     from paper_1401_3615_b200 import synth
 
     def measure(geom, mode_id, steps, slab):
         zz0, zz1 = slab
         LL = geom.edge_voxels
-        v2 = torch.empty(((zz1 - zz0), LL, LL), dtype=torch.float32, device=dev)
         o2 = pkg.Options(batch=args.batch, mode=mode_id)
-
-        b2 = pkg.row_band_for_slab(geom, W, H, zz0, zz1, mats)
+        s2 = SlabStep(pkg, torch, dev, geom, imgs, mats, zz0, zz1, o2, err, stream,
+                      force_quad=args.quad)
+        v2 = s2.vol
 
         def st2():
             v2.zero_()
-            pkg.pack_device_band(imgs, b2, packed, err, stream)
-            pkg.backproject_device(v2, geom, zz0, zz1, packed, W, H, n, mats, o2, err, stream,
-                                   band=b2)
+            s2.prep()
+            s2.backproject()
         for _ in range(2):
             st2()
         if dist:
@@ -540,13 +600,14 @@ def secondary_entries(c):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         res = {"value": round(LL ** 3 * n / (ms * 1e-3) / 1e9, 3), "unit": "GUp/s",
-               "ms_per_step": round(ms, 3)}
+               "ms_per_step": round(ms, 3), "kernel": s2.kernel}
         if geom is g and mode_id != mode:
             # full-size agreement of the two modes on the GPU (exact mode is
             # bitwise the reference's result, see tests/test_gpu_parity.py)
             dff = pkg.compare_volumes_device(v2, vol)
             res["vs_exact" if mode_id == pkg.MODE_FAST else "vs_fast"] = {
                 k: dff[k] for k in ("rel_l2", "max_abs_over_range", "bitwise_different")}
+        s2.release()
         del v2
         return res
 
@@ -786,25 +847,26 @@ def config4_entry(c):
     g, mats, imgs = synth.make_inputs(cfg, device=dev, chunk=16)
     L = g.edge_voxels
     n, H, W = imgs.shape
-    nb = pkg.packed_layout(W, H)[2]
-    packed = torch.empty(n * nb, dtype=torch.uint8, device=dev)
-    vol = torch.empty((L, L, L), dtype=torch.float32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = c.stream
     res = {"workload": cfg.name, "edge_voxels": L, "projections": n, "detector": [W, H],
            "mode": args.mode}
+    sst = SlabStep(pkg, torch, dev, g, imgs, mats, 0, L, pkg.Options(batch=16, mode=c.mode),
+                   err, stream, force_quad=args.quad)
+    vol = sst.vol
+    res["kernel"] = sst.kernel
     for batch in (16, 32):
-        opt = pkg.Options(batch=batch, mode=c.mode)
+        sst.opt = pkg.Options(batch=batch, mode=c.mode)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
         def step(rec=False):
             vol.zero_()
             if rec:
                 ev[0].record(stream)
-            pkg.pack_device(imgs, packed, stream)
+            sst.prep()
             if rec:
                 ev[1].record(stream)
-            pkg.backproject_device(vol, g, 0, L, packed, W, H, n, mats, opt, err, stream)
+            sst.backproject()
             if rec:
                 ev[2].record(stream)
         step()
@@ -825,13 +887,14 @@ def config4_entry(c):
         frac = upd * OPS_PER_UPDATE / (launch_ms * 1e-3) / (nsm * 128 * sm_max * 1e6)
         res[f"batch{batch}"] = {"value": round(L ** 3 * n / (ms * 1e-3) / 1e9, 3),
                                 "unit": "GUp/s", "ms_per_step": round(ms, 2),
-                                "pack_ms": round(statistics.mean(pk), 2),
+                                "prep_ms": round(statistics.mean(pk), 2),
                                 "roofline_frac": round(frac, 4)}
     if int(err.item()) != 0:
         res["error_flag"] = int(err.item())
     res["value"] = res["batch16"]["value"]
     imgs_h = imgs.cpu().pin_memory()
-    del imgs, packed, vol
+    sst.release()
+    del imgs, vol
     torch.cuda.empty_cache()
     imgs_np = imgs_h.numpy()
     vol_h = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
