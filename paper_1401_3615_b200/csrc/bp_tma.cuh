@@ -99,6 +99,20 @@ __device__ __forceinline__ unsigned atom_add_shared(unsigned addr, unsigned v) {
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
     return old;
 }
+__device__ __forceinline__ void mbar_arrive_a(unsigned addr) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_test_a(unsigned addr, unsigned parity) {
+    unsigned r;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(r)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return r != 0u;
+}
 // Non-blocking probe: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
     unsigned r;
@@ -329,7 +343,8 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     const int stage_floats = PITCH * args.bh;
     float* stages = reinterpret_cast<float*>(tsm);
     __shared__ unsigned long long full[kTMaxStages];
-    __shared__ unsigned s_cnt[kTMaxStages]; // warps done with the slot's current use
+    __shared__ unsigned long long empty[kTMaxStages]; // one arrive per warp and use
+    __shared__ int s_claim[kTMaxStages];    // staged index whose refill was claimed
     __shared__ int s_tlist[kMaxBatch];      // staged projections in order
     __shared__ int2 s_box[kMaxBatch];
     __shared__ float s_bias[kMaxBatch];
@@ -440,7 +455,8 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            s_cnt[s] = 0u;
+            mbar_init(&empty[s], kTThreads / 32);
+            s_claim[s] = -1;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -483,7 +499,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 
     unsigned vmin = bigm ? 0u : ~0u;
     const unsigned sb0 = smem_u32(stages) + args.magic_off;
-    const unsigned full0 = smem_u32(full), cnt0 = smem_u32(s_cnt);
+    const unsigned full0 = smem_u32(full), empty0 = smem_u32(empty);
     unsigned sbc = sb0;      // biased shared address of the consumer's slot
     int k = 0, cslot = 0;    // consumer position among the staged projections
     unsigned cph = 0u;       // parity of the consumer slot's current use
@@ -502,12 +518,15 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             __syncwarp();
             if (lane == 0) {
                 // the warp's reads of the slot are done (issued before, in
-                // order); the last of the 8 warps recycles the slot
-                if (atom_add_shared(cnt0 + 4u * (unsigned)cslot, 1u) == kTThreads / 32 - 1) {
-                    s_cnt[cslot] = 0u;
-                    if (k + S < ntma)
-                        issue(cslot, s_tlist[k + S]);
-                }
+                // order). Every warp arrives on the slot's empty barrier; a
+                // warp that then sees the phase complete (its own arrival
+                // was the last, or a concurrent one was) claims the refill
+                // -- normally one warp, so the claim's atomic is rare.
+                const unsigned eb = empty0 + 8u * (unsigned)cslot;
+                mbar_arrive_a(eb);
+                if (k + S < ntma && mbar_test_a(eb, cph) &&
+                    atomicExch(&s_claim[cslot], k) != k)
+                    issue(cslot, s_tlist[k + S]);
             }
             ++k;
             if (++cslot == S) {
