@@ -503,41 +503,48 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     unsigned sbc = sb0;      // biased shared address of the consumer's slot
     int k = 0, cslot = 0;    // consumer position among the staged projections
     unsigned cph = 0u;       // parity of the consumer slot's current use
-    for (unsigned rem = act; rem; rem &= rem - 1u) {
-        const int p = __ffs(rem) - 1;
-        const float* m = mats.a[p];
-        const f2* zuv = tabs.zuv + p * R;
-        const f2* zw = tabs.zw + p * (R / 2);
-        const bool mine = (todo >> p) & 1u;
-        if ((tma_mask >> p) & 1u) {
-            mbar_wait_a(full0 + 8u * (unsigned)cslot, cph);
-            if (mine) {
-                const SmemFetch<PITCH> f{sbc, s_bias[p]};
-                bp_project_f<R, MODE>(args, m, wx, wy, zuv, zw, accp, vmin, f);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                // the warp's reads of the slot are done (issued before, in
-                // order). Every warp arrives on the slot's empty barrier; a
-                // warp that then sees the phase complete (its own arrival
-                // was the last, or a concurrent one was) claims the refill
-                // -- normally one warp, so the claim's atomic is rare.
-                const unsigned eb = empty0 + 8u * (unsigned)cslot;
-                mbar_arrive_a(eb);
-                if (k + S < ntma && mbar_test_a(eb, cph) &&
-                    atomicExch(&s_claim[cslot], k) != k)
-                    issue(cslot, s_tlist[k + S]);
-            }
-            ++k;
-            if (++cslot == S) {
-                cslot = 0;
-                cph ^= 1u;
-                sbc = sb0;
-            } else {
-                sbc += stage_bytes;
-            }
-        } else if (mine) {
-            bp_project_f<R, MODE>(args, m, wx, wy, zuv, zw, accp, vmin, raw_fetch(args, p));
+    // one staged projection: wait for its box, compute (if this warp's tile
+    // touches it), release the slot
+    auto staged = [&](int p) {
+        mbar_wait_a(full0 + 8u * (unsigned)cslot, cph);
+        if ((todo >> p) & 1u) {
+            const SmemFetch<PITCH> f{sbc, s_bias[p]};
+            bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
+                                  tabs.zw + p * (R / 2), accp, vmin, f);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // the warp's reads of the slot are done (issued before, in
+            // order). Every warp arrives on the slot's empty barrier; a warp
+            // that then sees the phase complete (its own arrival was the
+            // last, or a concurrent one was) claims the refill -- normally
+            // one warp, so the claim's atomic is rare.
+            const unsigned eb = empty0 + 8u * (unsigned)cslot;
+            mbar_arrive_a(eb);
+            if (k + S < ntma && mbar_test_a(eb, cph) && atomicExch(&s_claim[cslot], k) != k)
+                issue(cslot, s_tlist[k + S]);
+        }
+        ++k;
+        if (++cslot == S) {
+            cslot = 0;
+            cph ^= 1u;
+            sbc = sb0;
+        } else {
+            sbc += stage_bytes;
+        }
+    };
+    if (act == tma_mask) {
+        // common case: every active projection is staged
+        for (int t = 0; t < ntma; ++t)
+            staged(s_tlist[t]);
+    } else {
+        for (unsigned rem = act; rem; rem &= rem - 1u) {
+            const int p = __ffs(rem) - 1;
+            if ((tma_mask >> p) & 1u)
+                staged(p);
+            else if ((todo >> p) & 1u)
+                bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
+                                      tabs.zw + p * (R / 2), accp, vmin, raw_fetch(args, p));
         }
     }
     bool redo = false;
