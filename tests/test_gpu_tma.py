@@ -180,7 +180,23 @@ def test_pipeline_raw_mode(scan, expected, monkeypatch, resident):
     assert bits_equal(vq, expected)
     # both count only provably-zero (culled) updates; the TMA kernel's warp
     # tiles differ from the quad kernel's, so the fractions are close, not equal
-    assert 0.0 < st["culled_fraction"] and abs(st["culled_fraction"] - stq["culled_fraction"]) < 0.1
+    assert abs(st["culled_fraction"] - stq["culled_fraction"]) < 0.1
+
+
+def test_pipeline_raw_mode_off_centre_culling(scan, oracle):
+    """An off-centre sub-cube reaching past the detector edge: culling skips
+    part of the work (counted), results stay bitwise."""
+    g0, mats, imgs = scan
+    g = VolumeGeometry(L, g0.voxel_mm, 60.0)  # x, y, z from 60 mm to 107.5 mm
+    host = imgs.cpu().numpy()
+    ref = np.zeros((L, L, L), np.float32)
+    assert oracle.reconstruct(ref, g, host, mats) == 0
+    n, H, W = host.shape
+    assert pkg.tma_plan(g, W, H, 0, L, mats)["staged"] == 1
+    v = np.zeros((L, L, L), np.float32)
+    st = pkg.reconstruct_arrays(v, g, host, mats, pkg.Options(num_gpus=1, count_culled=True))
+    assert bits_equal(v, ref)
+    assert st["culled_fraction"] > 0.01
 
 
 def test_pipeline_raw_mode_filter_and_nan(scan, oracle, monkeypatch):
