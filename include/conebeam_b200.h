@@ -73,7 +73,7 @@ enum {
 
 /* Options (the B200 counterpart of cb_opt_options, capi.h:84-91). */
 typedef struct cbb_options {
-    int32_t num_gpus;          /* 0 = all visible devices (whole-stack calls) */
+    int32_t num_gpus;          /* default 1; 0 = all visible devices (whole-stack calls) */
     const int32_t* device_ids; /* nullable: devices 0..num_gpus-1; else num_gpus ids
                                   (num_gpus must then be > 0: it is the array length) */
     int32_t batch;             /* projections per kernel launch, 1..32 (default 32) */

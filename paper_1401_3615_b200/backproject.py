@@ -37,7 +37,7 @@ class Options:
     """cbb_options (include/conebeam_b200.h); B200 counterpart of OptOptions
     (proj/include/conebeam/kernel_opt.hpp:121-133)."""
 
-    num_gpus: int = 0                 # 0 = all visible devices
+    num_gpus: int = 1                 # 0 = all visible devices
     device_ids: Optional[Sequence[int]] = None
     batch: int = 32                   # projections per launch (1..32)
     mode: int = MODE_EXACT
@@ -55,8 +55,7 @@ class Options:
         if self.device_ids is not None:
             keep = (C.c_int32 * len(self.device_ids))(*[int(d) for d in self.device_ids])
             o.device_ids = C.cast(keep, C.POINTER(C.c_int32))
-            if self.num_gpus == 0:
-                o.num_gpus = len(self.device_ids)
+            o.num_gpus = len(self.device_ids)  # the C ABI reads num_gpus ids
         o.batch = int(self.batch)
         o.mode = int(self.mode)
         o.cull = int(bool(self.cull))

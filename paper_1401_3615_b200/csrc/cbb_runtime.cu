@@ -93,7 +93,9 @@ uint64_t cbb_launch_count(void) { return g_launches; }
 void cbb_options_defaults(cbb_options* o) {
     if (!o)
         return;
-    o->num_gpus = 0;
+    // one GPU unless asked: the cross-device paths (P2P band packs, rotating
+    // upload roots) are tested with several workers on one GPU only
+    o->num_gpus = 1;
     o->device_ids = nullptr;
     o->batch = 32;
     o->mode = CBB_MODE_EXACT;

@@ -451,9 +451,25 @@ struct Pipeline {
         slot = (slot + 1) % nslots;
     }
 
+    // host time spent issuing batches (CBB_TRACE: printed per call), the
+    // single-thread issue cost that bounds a multi-GPU batch rate
+    double issue_ms_sum = 0.0, issue_ms_max = 0.0;
+    uint64_t issue_count = 0;
+
     void issue(const float* src, const double* mats, int n, int stage = -1) {
+        const auto t0 = std::chrono::steady_clock::now();
         if (raw_mode)
-            return issue_raw(src, mats, n, stage);
+            issue_raw(src, mats, n, stage);
+        else
+            issue_packed(src, mats, n, stage);
+        const double ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        issue_ms_sum += ms;
+        issue_ms_max = std::max(issue_ms_max, ms);
+        ++issue_count;
+    }
+
+    void issue_packed(const float* src, const double* mats, int n, int stage) {
         NvtxRange range("cbb batch");
         const size_t bytes = raw_bytes_per_proj * n;
         // Batch k is uploaded once, by the root worker k mod G. Each other
@@ -874,6 +890,13 @@ struct Pipeline {
     void finish(float* vol_out) {
         NvtxRange range("cbb finish");
         flush();
+        if (std::getenv("CBB_TRACE") && issue_count)
+            std::fprintf(stderr,
+                         "cbb: %d worker(s), %s mode: %llu batches issued, host issue %.3f ms "
+                         "mean / %.3f ms max per batch\n",
+                         (int)workers.size(), raw_mode ? "raw" : "packed",
+                         (unsigned long long)issue_count, issue_ms_sum / issue_count,
+                         issue_ms_max);
         const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
         if (resident) {
             finish_resident(vol_out);

@@ -336,7 +336,7 @@ def test_abi_rejects_invalid_inputs_before_touching_the_gpu():
     assert call(v=None)[0] == 1 and "null" in call(v=None)[1]
     assert call(im=None)[0] == 1
     ids = (C.c_int32 * 1)(0)
-    assert call(opt={"device_ids": C.cast(ids, C.POINTER(C.c_int32))}) == (
+    assert call(opt={"device_ids": C.cast(ids, C.POINTER(C.c_int32)), "num_gpus": 0}) == (
         1, "options: device_ids needs num_gpus > 0 (its length)")
     assert np.all(vol == 7.0)
 
@@ -379,3 +379,17 @@ def test_tma_plan_for_baseline_configs(monkeypatch):
     assert pkg.tma_plan(cfg.geometry, 1247, 960, 0, 512, m)["staged"] == 0
     monkeypatch.setenv("CBB_BP_PATH", "quad")
     assert pkg.tma_plan(cfg.geometry, 1248, 960, 0, 512, m)["staged"] == 0
+
+
+def test_options_default_to_one_gpu():
+    """cbb_options_defaults: one GPU unless asked (the cross-device paths are
+    tested with several workers on one GPU only), exact mode, batch 32."""
+    import ctypes as C
+
+    from paper_1401_3615_b200 import _lib
+
+    oc = _lib.OptionsC()
+    _lib.lib().cbb_options_defaults(C.byref(oc))
+    assert (oc.num_gpus, oc.batch, oc.mode, oc.cull) == (1, 32, 0, 1)
+    o, _keep = pkg.Options(device_ids=[0, 0]).to_c()
+    assert o.num_gpus == 2
