@@ -479,18 +479,26 @@ struct Pipeline {
         // copies the band rows (cudaMemcpy3DPeerAsync) and packs locally.
         const int G = (int)workers.size();
         Worker& root = *workers[nbatch % G];
-        // raw[slot] of worker w may still be read by its own pack of batch
-        // k-nslots and, if w was that batch's root, by the other workers'
-        // band copies (h2d_done) or peer packs (raw_free)
-        for (auto& w : workers) {
-            CK(cudaSetDevice(w->device));
-            CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
-            for (auto& o : workers)
-                if (o != w) {
-                    CK(cudaStreamWaitEvent(w->copy, o->h2d_done[slot], 0));
-                    CK(cudaStreamWaitEvent(w->copy, o->raw_free[slot], 0));
-                }
+        // Slot reuse. The root's raw[slot] may still be read by the previous
+        // batch that used it: every worker's pack (peer packs read it
+        // directly; all record raw_free[slot]) and the other workers' band
+        // copies out of it (recorded as their h2d_done[slot]). A non-root
+        // worker writes only its own raw[slot], and only on the band-copy
+        // path, after its own pack of that slot's previous use (raw_free).
+        // About 3G stream-event waits per batch (was G(2G-1): 120 at G = 8,
+        // 0.17 ms of host issue time per batch, profiles/issue_time_r2.txt).
+        CK(cudaSetDevice(root.device));
+        for (auto& o : workers) {
+            CK(cudaStreamWaitEvent(root.copy, o->raw_free[slot], 0));
+            if (o.get() != &root)
+                CK(cudaStreamWaitEvent(root.copy, o->h2d_done[slot], 0));
         }
+        if (!peer_pack)
+            for (auto& w : workers)
+                if (w.get() != &root) {
+                    CK(cudaSetDevice(w->device));
+                    CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
+                }
         CK(cudaSetDevice(root.device));
         CK(cudaMemcpyAsync(root.d_raw[slot], src, bytes, cudaMemcpyHostToDevice, root.copy));
         CK(cudaEventRecord(root.h2d_done[slot], root.copy));
