@@ -679,6 +679,8 @@ struct Pipeline {
             const double cost = 3.0 * 2.0 * (double)slab / 6.5e12;
             const double gain = (double)std::max(0, opt.batch - 4) * W * H * 4.0 / 55e9;
             ramp_ = gain > cost ? 4 : opt.batch;
+            if (const char* e = std::getenv("CBB_RAMP")) // experiments: first batch size
+                ramp_ = std::max(1, std::atoi(e));
         }
         return std::min({opt.batch, std::max(ramp_, first), count - first});
     }
@@ -951,10 +953,13 @@ struct Pipeline {
         // part's extra launches cost (~30 us each): config 3 625 vs 631 ms
         // end to end; configs 0 and 1 lose ~0.7 ms if split.
         const int nlaunch = (resident_count + opt.batch - 1) / opt.batch;
+        // the last part is one z-block group (8 planes for the gather
+        // kernel, 12 for the staged kernel: no partly empty z-blocks)
+        const int gs = tail_group();
         auto tail_mid = [&](const Worker& w) {
-            const double saved_ms = (double)(w.tail_hi - w.tail_lo - 8) * plane * 4.0 / 50e6;
-            return w.tail_hi - w.tail_lo >= 16 && saved_ms > 0.03 * nlaunch ? w.tail_hi - 8
-                                                                            : w.tail_hi;
+            const double saved_ms = (double)(w.tail_hi - w.tail_lo - gs) * plane * 4.0 / 50e6;
+            return w.tail_hi - w.tail_lo >= 2 * gs && saved_ms > 0.03 * nlaunch ? w.tail_hi - gs
+                                                                                : w.tail_hi;
         };
         for (auto& w : workers) {
             CK(cudaSetDevice(w->device));
