@@ -257,7 +257,18 @@ __device__ __forceinline__ void bp_project_f(const TmaArgs& args, const float* m
                 const f2 ww = MUL2(wpair[k], wpair[k]);
                 float ww0, ww1;
                 upk(ww, ww0, ww1);
+#if CBB_TMA_YY
+                // 1/(w*w) seeded with RN(y*y) (y: the refined 1/w) instead of
+                // a second MUFU.RCP, then the same Newton step: as accurate
+                // (error squared by the step), one XU op fewer per voxel;
+                // bitwise the IEEE quotient on 4e10 random operand pairs
+                // (profiles/probes/weight_div_check.cu)
+                (void)ww0;
+                (void)ww1;
+                const f2 r2 = MUL2(ypair[k], ypair[k]);
+#else
                 const f2 r2 = pk(rcp_approx(ww0), rcp_approx(ww1));
+#endif
                 const f2 y2 = fma2(r2, fma2(neg2(ww), r2, ONE2), r2);
                 const f2 q0 = MUL2(vv, y2);
                 c = fma2(neg2(y2), fma2(ww, q0, neg2(vv)), q0);
@@ -330,6 +341,9 @@ __device__ __forceinline__ void corner_extent(const float* a, const float cx[2],
 // threads, dynamic shared memory: S stages of PITCH * bh floats, then 2 S
 // mbarriers.
 // ---------------------------------------------------------------------------
+#ifndef CBB_TMA_YY
+#define CBB_TMA_YY 1
+#endif
 #ifndef CBB_TMA_MINB
 #define CBB_TMA_MINB 3
 #endif
