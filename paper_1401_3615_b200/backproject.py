@@ -417,15 +417,28 @@ def scan_device(raw, flags, err_flag=None, stream=None) -> None:
     projections (contiguous CUDA float32 (N, rows, W))."""
     import torch
 
-    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
-        raise ValidationError("scan_device: raw must be a contiguous CUDA float32 (N, R, W) tensor")
+    stride = _rows_view_stride(raw, "scan_device")
     n, rows, w = raw.shape
     if flags.numel() * flags.element_size() < 4 * n:
         raise ValidationError("scan_device: flags too small")
     s = stream if stream is not None else torch.cuda.current_stream(raw.device)
     err = None if err_flag is None else err_flag.data_ptr()
-    _lib.check(_lib.lib().cbb_scan_device(raw.data_ptr(), rows * w, w, rows, n, flags.data_ptr(),
+    _lib.check(_lib.lib().cbb_scan_device(raw.data_ptr(), stride, w, rows, n, flags.data_ptr(),
                                           err, C.c_void_p(s.cuda_stream)))
+
+
+def _rows_view_stride(raw, what: str) -> int:
+    """(N, rows, W) CUDA float32 tensor whose rows are contiguous (a whole
+    stack, or a band of rows of one: raw[:, r0:r0 + rn]); returns the
+    projection stride in floats."""
+    import torch
+
+    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.dim() == 3):
+        raise ValidationError(f"{what}: raw must be a CUDA float32 (N, R, W) tensor")
+    n, rows, w = raw.shape
+    if raw.stride(2) != 1 or (rows > 1 and raw.stride(1) != w) or (n > 1 and raw.stride(0) < rows * w):
+        raise ValidationError(f"{what}: raw rows must be contiguous (a stack or a band of one)")
+    return int(raw.stride(0)) if n > 1 else rows * w
 
 
 def backproject_raw_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_end: int, raw,
@@ -433,16 +446,16 @@ def backproject_raw_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_e
                            options: Optional[Options] = None, err_flag=None, stream=None,
                            first: int = 0, band: Optional[RowBand] = None) -> None:
     """cbb_backproject_raw_device: back-projection straight from raw
-    projections (contiguous CUDA float32 (N, rows, W): the full detector, or
-    the band's rows with `band`), each block's footprint staged in shared
-    memory by TMA; `flags` from scan_device over the same projections.
-    Projections [first, first + count) of the tensor are used."""
+    projections (CUDA float32 (N, rows, W) with contiguous rows: the full
+    detector, or the band's rows with `band` -- e.g. raw[:, r0:r0 + rn] of a
+    full stack), each block's footprint staged in shared memory by TMA;
+    `flags` from scan_device over the same projections. Projections
+    [first, first + count) of the tensor are used."""
     import torch
 
     if not (vol_slab.is_cuda and vol_slab.dtype == torch.float32 and vol_slab.is_contiguous()):
         raise ValidationError("backproject_raw_device: vol_slab must be a contiguous CUDA float32 tensor")
-    if not (raw.is_cuda and raw.dtype == torch.float32 and raw.is_contiguous() and raw.dim() == 3):
-        raise ValidationError("backproject_raw_device: raw must be a contiguous CUDA float32 (N, R, W) tensor")
+    stride = _rows_view_stride(raw, "backproject_raw_device")
     L = geometry.edge_voxels
     if vol_slab.numel() < (z_end - z_begin) * L * L:
         raise ValidationError("backproject_raw_device: slab tensor too small")
@@ -454,7 +467,6 @@ def backproject_raw_device(vol_slab, geometry: VolumeGeometry, z_begin: int, z_e
     g = geometry_c(geometry)
     s = stream if stream is not None else torch.cuda.current_stream(vol_slab.device)
     err = None if err_flag is None else err_flag.data_ptr()
-    stride = rows * w
     _lib.check(_lib.lib().cbb_backproject_raw_device(
         vol_slab.data_ptr(), C.byref(g), int(z_begin), int(z_end),
         raw.data_ptr() + 4 * int(first) * stride, stride, int(width), int(height),

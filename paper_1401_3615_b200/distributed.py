@@ -111,12 +111,17 @@ def cuda_hooks(geometry: VolumeGeometry, width: int, height: int, options=None,
     the detector rows its slab projects onto (cbb_pack_device_band) and the
     kernel reads that band; for_stack picks the band for a stack."""
     from .backproject import (backproject_device, check_finite_device, pack_device,
-                              pack_device_band, packed_layout, row_band_for_slab)
+                              pack_device_band, packed_layout, row_band_for_slab, tma_plan)
 
     _, _, nb = packed_layout(width, height)
 
-    def for_stack(z0, z1, mats):
+    def for_stack(z0, z1, mats, staged=True):
+        # the TMA-staged raw hooks when the slab's footprint boxes fit (and
+        # the batch lives in local memory: staged=False for the IPC transport,
+        # whose packs read the uploader's slot over peer memory)
         b = row_band_for_slab(geometry, width, height, z0, z1, mats)
+        if staged and tma_plan(geometry, width, height, z0, z1, mats)["staged"]:
+            return raw_hooks(geometry, width, height, options, b, for_stack)
         return cuda_hooks(geometry, width, height, options, band=b)
 
     if band is None:
@@ -142,6 +147,37 @@ def cuda_hooks(geometry: VolumeGeometry, width: int, height: int, options=None,
     full = band.cell_row0 == 0 and band.cell_rows == packed_layout(width, height)[1]
     return Hooks(pack_b, back_b, band.packed_bytes(width, height), None if full else check,
                  for_stack)
+
+
+def raw_hooks(geometry: VolumeGeometry, width: int, height: int, options, band,
+              for_stack=None) -> Hooks:
+    """Hooks for the TMA-staged kernel (bp_tma.cuh): no packing. `pack` scans
+    the rank's band rows of the received batch (scan_projections: the
+    per-projection numerator flags, kept in the 'packed' buffer, 4 bytes per
+    projection) and `backproject` reads those rows straight from the raw
+    slot (a band view: rows [r0, r0 + rn) of each projection)."""
+    import torch
+
+    from .backproject import backproject_raw_device, check_finite_device, scan_device
+
+    state = {}
+    r0, rn = band.raw_row0, band.raw_rows
+
+    def pack(raw, packed, err):
+        view = raw[:, r0:r0 + rn]
+        flags = packed[:4 * raw.shape[0]].view(torch.int32)
+        scan_device(view, flags, err)
+        state["raw"], state["flags"] = view, flags
+
+    def back(vol_slab, z0, z1, packed, n, mats, err):
+        backproject_raw_device(vol_slab, geometry, z0, z1, state["raw"], width, height, n, mats,
+                               state["flags"], options, err_flag=err, band=band)
+
+    def check(raw, err):
+        check_finite_device(raw, err)
+
+    full = r0 == 0 and rn == height
+    return Hooks(pack, back, 4, None if full else check, for_stack)
 
 
 class DistributedReconstructor:
@@ -344,7 +380,10 @@ class DistributedReconstructor:
         count = m.shape[0]
         hooks = self.hooks
         if hooks.for_stack is not None:
-            hooks = hooks.for_stack(self.z0, self.z1, m)
+            if self.transport == "ipc":
+                hooks = hooks.for_stack(self.z0, self.z1, m, staged=False)
+            else:
+                hooks = hooks.for_stack(self.z0, self.z1, m)
             if hooks.packed_bytes > self.hooks.packed_bytes:
                 raise ValueError("stack hooks need larger packed buffers")
         if initial_slab is not None:
