@@ -30,6 +30,7 @@
 #pragma once
 
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -308,6 +309,251 @@ ramp_fft_rows(const float* raw, float* out, int W, long long rows,
     }
 }
 
+// ---------------------------------------------------------------------------
+// N = 2560 = 10 x 16 x 16 for detectors up to 1280 pixels (BASELINE configs
+// 0-3: W = 1248): 0.59x the FP64 work of N = 4096. Mixed-radix Stockham,
+// forward passes radix 10, 16, 16 and inverse passes 16, 16, 10, so the
+// forward transform's last pass (radix 16, thread j < 160 holds
+// Z[j + 160 q]) is again exactly the inverse's first pass, in registers, and
+// the inverse's last pass (radix 10, stride 256) hands thread j the outputs
+// y[j + 256 q] -- the same store pattern as the N = 4096 kernel.
+// ---------------------------------------------------------------------------
+constexpr int kRf2N = 2560;
+constexpr int kRf2T16 = kRf2N / 16; // 160 threads in the radix-16 passes
+constexpr int kRf2MaxW = 1280;      // N >= 2W - 1 and W <= 5 * 256
+
+// 5-point DFT in place (forward W5 = exp(-2 pi i / 5); inverse conjugate).
+template <bool INV>
+__device__ __forceinline__ void dft5(cd& x0, cd& x1, cd& x2, cd& x3, cd& x4) {
+    constexpr double C1 = 0.30901699437494745, C2 = -0.80901699437494742;
+    constexpr double S1 = 0.95105651629515357, S2 = 0.58778525229247314;
+    const cd t1 = x1 + x4, t2 = x2 + x3, t3 = x1 - x4, t4 = x2 - x3;
+    const cd a1{fma(C2, t2.x, fma(C1, t1.x, x0.x)), fma(C2, t2.y, fma(C1, t1.y, x0.y))};
+    const cd a2{fma(C1, t2.x, fma(C2, t1.x, x0.x)), fma(C1, t2.y, fma(C2, t1.y, x0.y))};
+    const cd b1{fma(S2, t4.x, S1 * t3.x), fma(S2, t4.y, S1 * t3.y)};
+    const cd b2{fma(-S1, t4.x, S2 * t3.x), fma(-S1, t4.y, S2 * t3.y)};
+    // forward: X1 = a1 - i b1, X4 = a1 + i b1, X2 = a2 - i b2, X3 = a2 + i b2
+    const cd ib1 = INV ? cd{-b1.y, b1.x} : cd{b1.y, -b1.x}; // -+ i b1
+    const cd ib2 = INV ? cd{-b2.y, b2.x} : cd{b2.y, -b2.x};
+    x0 = x0 + t1 + t2;
+    x1 = a1 + ib1;
+    x4 = a1 - ib1;
+    x2 = a2 + ib2;
+    x3 = a2 - ib2;
+}
+
+// v *= W10^e (forward exp(-2 pi i e / 10), inverse conjugate), 1 <= e <= 4.
+template <bool INV, int E>
+__device__ __forceinline__ void w10(cd& v) {
+    constexpr double C[5] = {1.0, 0.80901699437494745, 0.30901699437494742,
+                             -0.30901699437494734, -0.80901699437494734};
+    constexpr double S[5] = {0.0, 0.58778525229247314, 0.95105651629515357,
+                             0.95105651629515364, 0.58778525229247325};
+    const double c = C[E], sn = INV ? -S[E] : S[E];
+    // (x + i y)(c - i s) = (x c + y s) + i (y c - x s)
+    v = cd{fma(v.x, c, v.y * sn), fma(v.y, c, -v.x * sn)};
+}
+
+// 10-point DFT of v[0..9] as 2 x 5 (n = 5 n1 + n2, k = k1 + 2 k2); output
+// X[k] lands in v[5 (k % 2) + k / 2]. ZHI: inputs v[5..9] are zero (the
+// zero-padded half of the forward transform's first pass).
+template <bool INV, bool ZHI>
+__device__ __forceinline__ void dft10(cd (&v)[16]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 5; ++n2) {
+        if (ZHI) {
+            v[5 + n2] = v[n2];
+        } else {
+            const cd a = v[n2], b = v[5 + n2];
+            v[n2] = a + b;
+            v[5 + n2] = a - b;
+        }
+    }
+    w10<INV, 1>(v[6]);
+    w10<INV, 2>(v[7]);
+    w10<INV, 3>(v[8]);
+    w10<INV, 4>(v[9]);
+    dft5<INV>(v[0], v[1], v[2], v[3], v[4]);
+    dft5<INV>(v[5], v[6], v[7], v[8], v[9]);
+}
+__device__ __forceinline__ constexpr int x10(int k) { return 5 * (k % 2) + k / 2; }
+
+// smem layout of the N = 2560 kernel: plane, spectrum (N/2 + 1 -> N/2 + 2),
+// twiddle bases tw[0..256), tw[16 m] (m < 10), tw[10 m] (m < 16), then two
+// prefetch stages of two 1280-float rows
+constexpr int kRf2Bytes = kRf2N * 16 + (kRf2N / 2 + 2) * 8 + (256 + 10 + 16) * 16 +
+                          2 * 2 * kRf2MaxW * 4; // 76208 B
+
+template <bool INV, int NS>
+__device__ __forceinline__ void rf2_twiddle16(cd (&v)[16], cd w1) {
+    if (INV)
+        w1.y = -w1.y;
+    cd w = w1;
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        v[r] = cmul(v[r], w);
+        if (r < 15)
+            w = cmul(w, w1);
+    }
+}
+
+__global__ void __launch_bounds__(kRfT, 2)
+ramp_fft2560_rows(const float* raw, float* out, int W, long long rows,
+                  const double* __restrict__ spec, const double2* __restrict__ tw) {
+    extern __shared__ double2 rf_smem[];
+    double2* buf = rf_smem;
+    double* hs = reinterpret_cast<double*>(rf_smem + kRf2N);
+    double2* tw256 = reinterpret_cast<double2*>(hs + kRf2N / 2 + 2);
+    double2* tw16x = tw256 + 256; // tw[16 m], m < 10: forward radix-16 pass, Ns = 10
+    double2* tw10x = tw16x + 10;  // tw[10 m], m < 16: inverse radix-16 pass, Ns = 16
+    float* stg = reinterpret_cast<float*>(tw10x + 16);
+    constexpr int SROW = kRf2MaxW;
+    const int j = threadIdx.x;
+    const bool act16 = j < kRf2T16; // the radix-16 passes use 160 threads
+    for (int k = j; k <= kRf2N / 2; k += kRfT)
+        hs[k] = spec[k];
+    tw256[j] = __ldg(tw + j);
+    if (j < 10)
+        tw16x[j] = __ldg(tw + 16 * j);
+    if (j < 16)
+        tw10x[j] = __ldg(tw + 10 * j);
+    const long long pairs = (rows + 1) / 2;
+    auto prefetch = [&](long long p, int s) {
+        if (p < pairs) {
+            const float* r1 = raw + (2 * p) * (long long)W;
+            const int nrow = 2 * p + 1 < rows ? 2 : 1;
+            for (int e = j; e < nrow * W; e += kRfT) {
+                const int row = e >= W, n = e - row * W;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(stg + (2 * s + row) * SROW + n);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(r1 + e));
+            }
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    prefetch(blockIdx.x, 0);
+    __syncthreads();
+    int s = 0;
+    for (long long p = blockIdx.x; p < pairs; p += gridDim.x, s ^= 1) {
+        const bool two = 2 * p + 1 < rows;
+        cd v[16];
+        prefetch(p + gridDim.x, s ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        {
+            const float* a = stg + 2 * s * SROW;
+#pragma unroll
+            for (int r = 0; r < 10; ++r) {
+                const int n = j + r * kRfT;
+                const bool in = r < 5 && n < W;
+                v[r] = cd{in ? (double)a[n] : 0.0, (in && two) ? (double)a[SROW + n] : 0.0};
+            }
+        }
+        // forward A: radix 10, Ns = 1 (256 threads): -> buf[10 j + q]
+        dft10<false, true>(v);
+#pragma unroll
+        for (int q = 0; q < 10; ++q)
+            buf[rf_sw(10 * j + q)] = make_double2(v[x10(q)].x, v[x10(q)].y);
+        __syncthreads();
+        // forward B: radix 16, Ns = 10
+        if (act16) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+                v[r] = cd{x.x, x.y};
+            }
+        }
+        __syncthreads();
+        if (act16) {
+            const double2 t = tw16x[j % 10];
+            rf2_twiddle16<false, 10>(v, cd{t.x, t.y});
+            dft16<false>(v);
+            const int base = (j / 10) * 160 + (j % 10);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(base + 10 * q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // forward C: radix 16, Ns = 160 -> registers: v[q] = Z[j + 160 q]
+        if (act16) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+                v[r] = cd{x.x, x.y};
+            }
+        }
+        __syncthreads();
+        if (act16) {
+            const double2 t = tw256[j];
+            rf2_twiddle16<false, 160>(v, cd{t.x, t.y});
+            dft16<false>(v);
+            cd o[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                o[q] = v[x16(q)];
+            // spectrum multiply, then inverse A: radix 16, Ns = 1 -> buf[16 j + q]
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k = j + kRf2T16 * q;
+                const double h = hs[k <= kRf2N / 2 ? k : kRf2N - k];
+                v[q] = cd{o[q].x * h, o[q].y * h};
+            }
+            dft16<true>(v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(16 * j + q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // inverse B: radix 16, Ns = 16
+        if (act16) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+                v[r] = cd{x.x, x.y};
+            }
+        }
+        __syncthreads();
+        if (act16) {
+            const double2 t = tw10x[j % 16];
+            rf2_twiddle16<true, 16>(v, cd{t.x, t.y});
+            dft16<true>(v);
+            const int base = (j / 16) * 256 + (j % 16);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(base + 16 * q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // inverse C: radix 10, Ns = 256 (256 threads): y[j + 256 q]
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const double2 x = buf[rf_sw(j + kRfT * r)];
+            v[r] = cd{x.x, x.y};
+        }
+        {
+            const double2 t = tw256[j];
+            const cd w1{t.x, -t.y};
+            cd w = w1;
+#pragma unroll
+            for (int r = 1; r < 10; ++r) {
+                v[r] = cmul(v[r], w);
+                if (r < 9)
+                    w = cmul(w, w1);
+            }
+        }
+        dft10<true, false>(v);
+        float* o1 = out + (2 * p) * (long long)W;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int n = j + q * kRfT;
+            if (n < W) {
+                o1[n] = (float)v[x10(q)].x;
+                if (two)
+                    o1[W + n] = (float)v[x10(q)].y;
+            }
+        }
+        __syncthreads(); // buf reused by the next pair's first pass
+    }
+}
+
 // spec[k] = (1/N) sum_n hc[n] cos(2 pi k n / N), hc the wrapped kernel
 // (n <= N/2: h(n), else h(n - N)); tw[e] = exp(-2 pi i e / N).
 __global__ void ramp_fft_tables(double* spec, double2* tw, int N, double tau) {
@@ -338,17 +584,17 @@ class RampFftCache {
         static RampFftCache c;
         return c;
     }
-    // tables for (device, tau); built once on stream st (synchronously)
-    RampFftTables tables(int device, double tau, cudaStream_t st) {
+    // tables for (device, tau, N); built once on stream st (synchronously)
+    RampFftTables tables(int device, double tau, cudaStream_t st, int N = kRfN) {
         std::lock_guard<std::mutex> lk(mu_);
-        auto key = std::make_tuple(device, tau);
+        auto key = std::make_tuple(device, tau, N);
         auto it = map_.find(key);
         if (it != map_.end())
             return it->second;
         RampFftTables t;
-        check_cuda(cudaMalloc(&t.spec, sizeof(double) * kRfN), "cudaMalloc(ramp spectrum)");
-        check_cuda(cudaMalloc(&t.tw, sizeof(double2) * kRfN), "cudaMalloc(ramp twiddles)");
-        ramp_fft_tables<<<kRfN / 128, 128, 0, st>>>(t.spec, t.tw, kRfN, tau);
+        check_cuda(cudaMalloc(&t.spec, sizeof(double) * N), "cudaMalloc(ramp spectrum)");
+        check_cuda(cudaMalloc(&t.tw, sizeof(double2) * N), "cudaMalloc(ramp twiddles)");
+        ramp_fft_tables<<<(N + 127) / 128, 128, 0, st>>>(t.spec, t.tw, N, tau);
         check_cuda(cudaGetLastError(), "ramp_fft_tables");
         check_cuda(cudaStreamSynchronize(st), "ramp_fft_tables");
         ++g_launches;
@@ -357,7 +603,7 @@ class RampFftCache {
 
   private:
     std::mutex mu_;
-    std::map<std::tuple<int, double>, RampFftTables> map_;
+    std::map<std::tuple<int, double, int>, RampFftTables> map_;
 };
 
 template <int NZ>
@@ -381,7 +627,6 @@ inline void ramp_fft_device(const float* raw, float* out, int W, int H, int coun
                             cudaStream_t st) {
     int dev = 0;
     check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
-    const RampFftTables t = RampFftCache::get().tables(dev, tau, st);
     const long long rows = (long long)H * count;
     const long long pairs = (rows + 1) / 2;
     int nsm = 148;
@@ -389,6 +634,23 @@ inline void ramp_fft_device(const float* raw, float* out, int W, int H, int coun
     const long long grid = std::min<long long>(pairs, (long long)nsm * 2); // 2 CTAs/SM
     if (grid < 1)
         return;
+    static const bool no2560 = std::getenv("CBB_RAMP_4096") != nullptr; // comparisons
+    if (W <= kRf2MaxW && !no2560) {
+        const RampFftTables t2 = RampFftCache::get().tables(dev, tau, st, kRf2N);
+        static bool attr2[64] = {};
+        if (dev < 64 && !attr2[dev]) {
+            check_cuda(cudaFuncSetAttribute(ramp_fft2560_rows,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kRf2Bytes),
+                       "cudaFuncSetAttribute(ramp_fft2560_rows)");
+            attr2[dev] = true;
+        }
+        ramp_fft2560_rows<<<(unsigned)grid, kRfT, kRf2Bytes, st>>>(raw, out, W, rows, t2.spec,
+                                                                  t2.tw);
+        check_cuda(cudaGetLastError(), "ramp_fft2560_rows");
+        ++g_launches;
+        return;
+    }
+    const RampFftTables t = RampFftCache::get().tables(dev, tau, st);
     const int nz = (W + kRfT - 1) / kRfT;
     if (nz <= 5)
         launch_ramp_fft<5>(dev, (unsigned)grid, raw, out, W, rows, t, st);
