@@ -38,7 +38,9 @@ constexpr int kTBX = 16, kTBY = 16;   // block tile in x, y (voxels)
 #define CBB_TMA_R 12
 #endif
 constexpr int kTR = CBB_TMA_R;        // voxels per thread along z
-constexpr int kGR = 8;                // guarded kernel: voxels per thread along z
+// guarded kernel: voxels per thread along z -- the same z-blocks as the staged
+// kernel, so a resident tail gap (aligned to kTR) maps identically
+constexpr int kGR = kTR;
 constexpr int kTThreads = 256;        // 8 warps of 8 x 4 voxel columns
 constexpr int kTMaxStages = 8;        // TMA ring depth limit (the host picks 2..8 stages)
 

@@ -278,6 +278,15 @@ struct Pipeline {
             }
             w->tail_lo = gz[best_i];
             w->tail_hi = gz[best_j];
+            if (const char* e = std::getenv("CBB_TAIL_PLANES")) { // tests: "lo:hi", group-aligned
+                int lo = 0, hi = 0;
+                if (std::sscanf(e, "%d:%d", &lo, &hi) == 2 && lo >= w->z_begin && hi <= w->z_end &&
+                    lo < hi && (lo - w->z_begin) % gs == 0 &&
+                    (hi == w->z_end || (hi - w->z_begin) % gs == 0)) {
+                    w->tail_lo = lo;
+                    w->tail_hi = hi;
+                }
+            }
             if (std::getenv("CBB_TRACE"))
                 std::fprintf(stderr, "cbb: device %d slab [%d, %d) tail [%d, %d)\n", w->device,
                              w->z_begin, w->z_end, w->tail_lo, w->tail_hi);
@@ -958,6 +967,8 @@ struct Pipeline {
         const int gs = tail_group();
         auto tail_mid = [&](const Worker& w) {
             const double saved_ms = (double)(w.tail_hi - w.tail_lo - gs) * plane * 4.0 / 50e6;
+            if (std::getenv("CBB_TAIL_NOSPLIT")) // experiments
+                return w.tail_hi;
             return w.tail_hi - w.tail_lo >= 2 * gs && saved_ms > 0.03 * nlaunch ? w.tail_hi - gs
                                                                                 : w.tail_hi;
         };

@@ -221,3 +221,23 @@ def test_pipeline_raw_mode_filter_and_nan(scan, oracle, monkeypatch):
     with pytest.raises(pkg.ValidationError, match="ProjectionImage contains non-finite"):
         pkg.reconstruct_arrays(v, g, bad, mats, pkg.Options(num_gpus=1))
     assert not v.any()
+
+
+@pytest.mark.parametrize("tail", [None, "12:36", "36:60"])
+def test_pipeline_raw_mode_guarded_batch_with_resident_tail(scan, oracle, monkeypatch, tail):
+    """A matrix with a -0.0 coefficient sends its batch to the guarded kernel
+    (bp_guarded_raw); in raw mode with the resident tail its head launch must
+    skip exactly the tail planes the staged kernel skips (same z-blocks, also
+    for tails that do not start at a multiple of 8 planes)."""
+    g, mats, imgs = scan
+    if tail:
+        monkeypatch.setenv("CBB_TAIL_PLANES", tail)
+    m = mats.copy()
+    m[9, 8] = -0.0  # a8 = -0: w no longer depends on z for projection 9
+    host = imgs.cpu().numpy()
+    ref = np.zeros((L, L, L), np.float32)
+    assert oracle.reconstruct(ref, g, host, m) == 0
+    v = np.zeros((L, L, L), np.float32)
+    st = pkg.reconstruct_arrays(v, g, host, m, pkg.Options(num_gpus=1, batch=8))
+    assert st["guarded_batches"] >= 1
+    assert bits_equal(v, ref)
