@@ -76,7 +76,9 @@ typedef struct cbb_options {
     int32_t num_gpus;          /* default 1; 0 = all visible devices (whole-stack calls) */
     const int32_t* device_ids; /* nullable: devices 0..num_gpus-1; else num_gpus ids
                                   (num_gpus must then be > 0: it is the array length) */
-    int32_t batch;             /* projections per kernel launch, 1..32 (default 32) */
+    int32_t batch;             /* projections per pipeline batch (upload + launch), 1..64
+                                  (default 32); the gather kernel launches at most 32 at a time,
+                                  the TMA-staged kernel up to 64 */
     int32_t mode;              /* CBB_MODE_EXACT / CBB_MODE_FAST */
     int32_t cull;              /* skip voxel tiles whose footprint misses the detector */
     int32_t volume_is_zero;    /* caller promises the input volume is all +0: skip its upload */

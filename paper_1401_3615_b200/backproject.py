@@ -39,7 +39,7 @@ class Options:
 
     num_gpus: int = 1                 # 0 = all visible devices
     device_ids: Optional[Sequence[int]] = None
-    batch: int = 32                   # projections per launch (1..32)
+    batch: int = 32                   # projections per pipeline batch (1..64)
     mode: int = MODE_EXACT
     cull: bool = True
     volume_is_zero: bool = False

@@ -66,6 +66,40 @@ struct TmaArgs {
                             // split it off the stage base into four load-address adds
 };
 
+constexpr int kTmaBatch = 64;         // projections per staged launch (64-bit masks)
+
+struct TmaMats {
+    float a[kTmaBatch][12]; // parameter-bank layout of bp_kernels.cuh (store_matrix)
+};
+
+// block_setup (bp_kernels.cuh) for up to kTmaBatch projections: the batch's
+// matrices and the block-uniform z-products in shared memory.
+template <int R>
+__device__ BlockTables<R> tma_block_setup(const TmaArgs& args, const TmaMats& mats, int zoff) {
+    __shared__ float s_m[kTmaBatch * 12];
+    __shared__ f2 s_zuv[kTmaBatch * R];
+    __shared__ f2 s_zw[kTmaBatch * (R / 2)];
+    const float* flat = &mats.a[0][0];
+    for (int i = threadIdx.x; i < args.count * 12; i += blockDim.x)
+        s_m[i] = flat[i];
+    const int z0 = args.z_begin + zoff, zl = args.z_end - 1;
+    for (int i = threadIdx.x; i < args.count * R; i += blockDim.x) {
+        const int p = i / R, r = i % R;
+        const float* a = flat + 12 * p;
+        const float wz = __fadd_rn(args.O, __fmul_rn((float)min(z0 + r, zl), args.MM));
+        s_zuv[i] = pk(__fmul_rn(wz, a[M67]), __fmul_rn(wz, a[M67 + 1]));
+    }
+    for (int i = threadIdx.x; i < args.count * (R / 2); i += blockDim.x) {
+        const int p = i / (R / 2), k = i % (R / 2);
+        const float wz0 = __fadd_rn(args.O, __fmul_rn((float)min(z0 + 2 * k, zl), args.MM));
+        const float wz1 = __fadd_rn(args.O, __fmul_rn((float)min(z0 + 2 * k + 1, zl), args.MM));
+        const float a8 = flat[12 * p + M8];
+        s_zw[i] = pk(__fmul_rn(wz0, a8), __fmul_rn(wz1, a8));
+    }
+    __syncthreads();
+    return BlockTables<R>{s_m, s_zuv, s_zw};
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier / TMA primitives
 // ---------------------------------------------------------------------------
@@ -352,7 +386,7 @@ __device__ __forceinline__ void corner_extent(const float* a, const float cx[2],
 template <int MODE, int PITCH, bool CNT>
 __global__ void __launch_bounds__(kTThreads, CBB_TMA_MINB)
 bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TmaArgs args,
-              const __grid_constant__ BpMats mats) {
+              const __grid_constant__ TmaMats mats) {
     constexpr int R = kTR, P = R / 2;
     extern __shared__ __align__(128) unsigned char tsm[];
     const int S = args.stages;
@@ -361,11 +395,11 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     __shared__ unsigned long long full[kTMaxStages];
     __shared__ unsigned long long empty[kTMaxStages]; // one arrive per warp and use
     __shared__ int s_claim[kTMaxStages];    // staged index whose refill was claimed
-    __shared__ int s_tlist[kMaxBatch];      // staged projections in order
-    __shared__ int2 s_box[kMaxBatch];
-    __shared__ float s_bias[kMaxBatch];
-    __shared__ unsigned s_fit;
-    __shared__ unsigned s_wmask[kTThreads / 32];
+    __shared__ int s_tlist[kTmaBatch];      // staged projections in order
+    __shared__ int2 s_box[kTmaBatch];
+    __shared__ float s_bias[kTmaBatch];
+    __shared__ unsigned long long s_fit;
+    __shared__ unsigned long long s_wmask[kTThreads / 32];
     __shared__ unsigned s_culled;
 
     const int lane = threadIdx.x & 31;
@@ -400,15 +434,15 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     }
     if (CNT && threadIdx.x == 0)
         s_culled = 0u;
-    const BlockTables<R> tabs = block_setup<R, false, TmaArgs>(args, mats, zoff);
+    const BlockTables<R> tabs = tma_block_setup<R>(args, mats, zoff);
     const float* s_m = tabs.m;
 
     // ---- per-warp culling (lane = projection) and per-block footprint boxes
     const int z0 = zfirst, z1 = min(zfirst + R - 1, args.z_end - 1);
     const float cz[2] = {O + (float)z0 * MM, O + (float)z1 * MM};
-    unsigned todo = 0u, bigm = 0u;
-    {
-        const int p = lane;
+    unsigned long long todo = 0ull, bigm = 0ull;
+    for (int half = 0; half < 2 && 32 * half < args.count; ++half) {
+        const int p = 32 * half + lane;
         bool active = false, big = false;
         if (p < args.count && tx0 < L && ty0 < L) {
             const float cx[2] = {O + (float)tx0 * MM, O + (float)min(tx0 + 7, L - 1) * MM};
@@ -423,15 +457,16 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         }
         if (MODE == 0 && p < args.count)
             big = (__ldg(args.flags + p) & 1u) != 0u;
-        todo = __ballot_sync(0xffffffffu, active);
-        bigm = __ballot_sync(0xffffffffu, big);
+        todo |= (unsigned long long)__ballot_sync(0xffffffffu, active) << (32 * half);
+        bigm |= (unsigned long long)__ballot_sync(0xffffffffu, big) << (32 * half);
     }
     if (!args.cull || __any_sync(0xffffffffu, negz))
-        todo = args.count == 32 ? ~0u : ((1u << args.count) - 1u);
+        todo = args.count == 64 ? ~0ull : ((1ull << args.count) - 1ull);
     if (warp == 0) {
-        // block box for projection `lane`: taps of every voxel of the tile
+      for (int half = 0; half < 2 && 32 * half < args.count; ++half) {
+        // block box for projection p: taps of every voxel of the tile
         // (padding voxels sit on real ones) lie in [floor(min ix), floor(max ix) + 2]
-        const int p = lane;
+        const int p = 32 * half + lane;
         bool fits = false;
         int bx0 = 0, by0 = 0;
         if (p < args.count) {
@@ -462,9 +497,11 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         s_box[p] = make_int2(bx0, by0);
         // SmemFetch bias: 2^23 - (by0 * PITCH + bx0), exact (|.| < 2^22)
         s_bias[p] = 8388608.0f - (float)(by0 * PITCH + bx0);
-        const unsigned fm = __ballot_sync(0xffffffffu, fits);
+        const unsigned long long fm = (unsigned long long)__ballot_sync(0xffffffffu, fits)
+                                      << (32 * half);
         if (lane == 0)
-            s_fit = fm;
+            s_fit = half ? (s_fit | fm) : fm;
+      }
     }
     if (lane == 0)
         s_wmask[warp] = todo;
@@ -478,13 +515,13 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    unsigned act = 0u;
+    unsigned long long act = 0ull;
 #pragma unroll
     for (int w = 0; w < kTThreads / 32; ++w)
         act |= s_wmask[w];
-    const unsigned tma_mask = act & s_fit;
+    const unsigned long long tma_mask = act & s_fit;
     const unsigned stage_bytes = (unsigned)stage_floats * 4u;
-    const int ntma = __popc(tma_mask);
+    const int ntma = __popcll(tma_mask);
     // Staged projection t (t-th bit of tma_mask) goes to slot t % S. Thread 0
     // fills the first S slots; afterwards the LAST warp to finish with a slot
     // (shared counter) refills it with projection t + S at once, so every
@@ -497,9 +534,9 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     b.y - args.raw_row0, args.tz0 + p);
     };
     if (threadIdx.x == 0) {
-        unsigned pm = tma_mask;
-        for (int t = 0; pm; ++t, pm &= pm - 1u) {
-            const int p = __ffs(pm) - 1;
+        unsigned long long pm = tma_mask;
+        for (int t = 0; pm; ++t, pm &= pm - 1ull) {
+            const int p = __ffsll(pm) - 1;
             s_tlist[t] = p;
             if (t < S)
                 issue(t, p);
@@ -508,7 +545,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     __syncthreads(); // s_tlist
     if (CNT) {
         const unsigned nv = __reduce_add_sync(0xffffffffu, (unsigned)nvalid);
-        const unsigned culled = (unsigned)args.count - __popc(todo);
+        const unsigned culled = (unsigned)args.count - __popcll(todo);
         if (lane == 0 && nv && culled)
             atomicAdd(&s_culled, nv * culled);
     }
@@ -523,7 +560,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     // touches it), release the slot
     auto staged = [&](int p) {
         mbar_wait_a(full0 + 8u * (unsigned)cslot, cph);
-        if ((todo >> p) & 1u) {
+        if ((todo >> p) & 1ull) {
             const SmemFetch<PITCH> f{sbc, s_bias[p]};
             bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
                                   tabs.zw + p * (R / 2), accp, vmin, f);
@@ -554,11 +591,11 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         for (int t = 0; t < ntma; ++t)
             staged(s_tlist[t]);
     } else {
-        for (unsigned rem = act; rem; rem &= rem - 1u) {
-            const int p = __ffs(rem) - 1;
-            if ((tma_mask >> p) & 1u)
+        for (unsigned long long rem = act; rem; rem &= rem - 1ull) {
+            const int p = __ffsll(rem) - 1;
+            if ((tma_mask >> p) & 1ull)
                 staged(p);
-            else if ((todo >> p) & 1u)
+            else if ((todo >> p) & 1ull)
                 bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
                                       tabs.zw + p * (R / 2), accp, vmin, raw_fetch(args, p));
         }
@@ -612,7 +649,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 // Grid (ceil(L/32), ceil(L/8), ceil(nz/R)), 256 threads.
 template <int MODE>
 __global__ void __launch_bounds__(256)
-bp_guarded_raw(const __grid_constant__ TmaArgs args, const __grid_constant__ BpMats mats) {
+bp_guarded_raw(const __grid_constant__ TmaArgs args, const __grid_constant__ TmaMats mats) {
     constexpr int R = kGR;
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const int y = blockIdx.y * 8 + (threadIdx.x >> 5);

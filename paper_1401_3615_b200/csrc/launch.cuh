@@ -223,8 +223,9 @@ uint64_t launch_backproject(float* vol_slab, const cbb_volume_geometry& g, int z
     const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, z_begin, z_end)};
     // CBB_FORCE_GUARDED (tests): run every batch through the guarded kernel
     const bool force_guarded = std::getenv("CBB_FORCE_GUARDED") != nullptr && err;
-    for (int first = 0; first < count; first += opt.batch) {
-        const int n = std::min(opt.batch, count - first);
+    const int per_launch = std::min(opt.batch, kMaxBatch);
+    for (int first = 0; first < count; first += per_launch) {
+        const int n = std::min(per_launch, count - first);
         BpMats m;
         bool safe = !force_guarded;
         for (int p = 0; p < n; ++p) {

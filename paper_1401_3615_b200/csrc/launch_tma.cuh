@@ -52,7 +52,7 @@ inline CUtensorMap raw_tensor_map(const float* raw, int W, int rows, long long s
 // Box widths the kernel is instantiated for (== 16 mod 32 floats: the rows
 // iy and iy + 1 of a warp's taps fall on shifted bank halves).
 constexpr int kPitches[] = {48, 80, 112, 144};
-constexpr int kTmaSmemBudget = 68 * 1024; // stages per block: 3 blocks/SM
+constexpr int kTmaSmemBudget = 60 * 1024; // stages per block: 3 blocks/SM (+13.5 KB static)
 constexpr int kTmaMinStages = 3;
 
 struct TmaPlan {
@@ -195,7 +195,7 @@ inline void launch_scan(const float* raw, int W, int rows, long long stride, int
 }
 
 template <int MODE, int PITCH>
-void launch_tma_kernel(const CUtensorMap& map, const TmaArgs& a, const BpMats& m, int nz,
+void launch_tma_kernel(const CUtensorMap& map, const TmaArgs& a, const TmaMats& m, int nz,
                        cudaStream_t st, bool cnt) {
     const size_t smem = (size_t)a.stages * PITCH * a.bh * 4;
     const dim3 grid((a.L + kTBX - 1) / kTBX, (a.L + kTBY - 1) / kTBY, (nz - a.gap + kTR - 1) / kTR);
@@ -214,7 +214,7 @@ void launch_tma_kernel(const CUtensorMap& map, const TmaArgs& a, const BpMats& m
 }
 
 template <int MODE>
-void launch_tma_pitch(const CUtensorMap& map, const TmaArgs& a, const BpMats& m, int nz,
+void launch_tma_pitch(const CUtensorMap& map, const TmaArgs& a, const TmaMats& m, int nz,
                       cudaStream_t st, bool cnt, int pitch) {
     switch (pitch) {
     case 48: return launch_tma_kernel<MODE, 48>(map, a, m, nz, st, cnt);
@@ -268,9 +268,12 @@ inline uint64_t launch_backproject_raw(float* vol_slab, const cbb_volume_geometr
     const double cmin[3] = {cxy, cxy, min_nonzero_coord(Of, MMf, z_begin, z_end)};
     const bool force_guarded = std::getenv("CBB_FORCE_GUARDED") != nullptr && err;
     uint64_t guarded = 0;
-    for (int first = 0; first < count; first += opt.batch) {
-        const int n = std::min(opt.batch, count - first);
-        BpMats m;
+    // launches of up to kTmaBatch projections (64-bit masks), whatever
+    // opt.batch (the pipeline's upload batch) is: the per-block setup and the
+    // slab's read-modify-write are amortised over more projections
+    for (int first = 0; first < count; first += kTmaBatch) {
+        const int n = std::min(kTmaBatch, count - first);
+        TmaMats m;
         bool safe = !force_guarded;
         for (int p = 0; p < n; ++p) {
             const double* am = mats + 12 * (size_t)(first + p);

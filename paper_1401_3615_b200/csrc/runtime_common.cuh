@@ -107,8 +107,8 @@ cbb_options resolve_options(const cbb_options* o) {
     cbb_options_defaults(&r);
     if (o)
         r = *o;
-    if (r.batch < 1 || r.batch > kMaxBatch)
-        fail(CBB_ERR_INVALID, "options: batch must be in [1, %d]", kMaxBatch);
+    if (r.batch < 1 || r.batch > kMaxOptBatch)
+        fail(CBB_ERR_INVALID, "options: batch must be in [1, %d]", kMaxOptBatch);
     if (r.mode != CBB_MODE_EXACT && r.mode != CBB_MODE_FAST)
         fail(CBB_ERR_INVALID, "options: unknown mode %d", r.mode);
     if (r.num_gpus < 0)

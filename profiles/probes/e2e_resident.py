@@ -20,7 +20,7 @@ imgs_h = imgs.pin_memory().numpy()
 L = g.edge_voxels
 vol_t = torch.zeros((L, L, L), dtype=torch.float32).pin_memory()
 vol = vol_t.numpy()
-opt = pkg.Options(volume_is_zero=True)
+opt = pkg.Options(volume_is_zero=True, batch=int(os.environ.get("BATCH", "32")))
 ref = None
 fracs = os.environ.get("FRACS", "0.06,0.09,0.11,0.14").split(",")
 for tag in ["plain"] + fracs:

@@ -329,7 +329,7 @@ def test_abi_rejects_invalid_inputs_before_touching_the_gpu():
     assert call(m=bad) == (1, "ProjectionMatrix: field 'a[7]' must be finite")
     assert call(geom=geometry_c(pkg.VolumeGeometry(0, 1.0, 0.0)))[0] == 1
     assert call(opt={"batch": 0})[0] == 1 and "batch" in call(opt={"batch": 0})[1]
-    assert call(opt={"batch": 33})[0] == 1
+    assert call(opt={"batch": 65})[0] == 1
     assert call(opt={"mode": 7})[0] == 1
     assert call(opt={"slab_begin": 5, "slab_end": 3})[0] == 1
     assert call(opt={"ramp_filter": 1, "filter_pixel_mm": 0.0})[0] == 1
