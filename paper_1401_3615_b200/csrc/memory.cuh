@@ -148,10 +148,22 @@ class HostPool {
 
 // Host copy into pinned staging, split over a few threads for large blocks
 // (a single thread moves ~5-10 GB/s, below the PCIe H2D rate).
+// Host threads for pageable <-> pinned copies: one memcpy stream reaches
+// only ~5-10 GB/s, so these copies (the drop-in's pageable volume and
+// per-image buffers) are spread over the host's cores; CBB_COPY_THREADS
+// overrides (default: all hardware threads, at most 32).
+inline unsigned copy_threads() {
+    static const unsigned n = [] {
+        if (const char* e = std::getenv("CBB_COPY_THREADS"))
+            return (unsigned)std::max(1, std::atoi(e));
+        return std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
+    }();
+    return n;
+}
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-    const size_t kChunk = size_t(8) << 20;
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(std::min<size_t>(hw, 8), (bytes + kChunk - 1) / kChunk);
+    const size_t kChunk = size_t(4) << 20;
+    const size_t nt = std::min<size_t>(copy_threads(), (bytes + kChunk - 1) / kChunk);
     if (nt <= 1) {
         std::memcpy(dst, src, bytes);
         return;
@@ -207,11 +219,22 @@ struct ChunkedXfer {
             return;
         }
         ensure();
+        const bool trace = std::getenv("CBB_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        double wait_ms = 0.0, copy_ms = 0.0;
+        auto ms_since = [](std::chrono::steady_clock::time_point a) {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a)
+                .count();
+        };
         int k = 0;
         for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
             const size_t len = std::min(kChunk, bytes - off);
+            auto ta = std::chrono::steady_clock::now();
             CK(cudaEventSynchronize(ev[k])); // buf[k]'s previous DMA finished
+            wait_ms += ms_since(ta);
+            ta = std::chrono::steady_clock::now();
             parallel_memcpy(buf[k], static_cast<const char*>(src) + off, len);
+            copy_ms += ms_since(ta);
             CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf[k], len,
                                cudaMemcpyHostToDevice, st));
             CK(cudaEventRecord(ev[k], st));
@@ -220,6 +243,10 @@ struct ChunkedXfer {
         // events are not): drain them before the next upload may refill them
         CK(cudaEventSynchronize(ev[0]));
         CK(cudaEventSynchronize(ev[1]));
+        if (trace)
+            std::fprintf(stderr, "cbb: pageable upload %.1f MB in %.2f ms (host copies %.2f ms, "
+                                 "waits %.2f ms)\n",
+                         bytes / 1e6, ms_since(t0), copy_ms, wait_ms);
     }
     // pageable dst: blocks until all bytes arrived; pinned dst: asynchronous
     void download(void* dst, const void* src, size_t bytes, cudaStream_t st, cudaEvent_t ev[2]) {

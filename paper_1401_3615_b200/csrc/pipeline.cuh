@@ -770,7 +770,7 @@ struct Pipeline {
             n = batch_at(first, count);
             wait_stage(sslot);
             float* dst = h_stage[sslot];
-            const int nt = (int)std::min<unsigned>(std::min(8u, hw), (unsigned)n);
+            const int nt = (int)std::min<unsigned>(copy_threads(), (unsigned)n);
             std::vector<std::thread> pool;
             for (int t = 0; t < nt; ++t)
                 pool.emplace_back([&, t] {
@@ -796,7 +796,7 @@ struct Pipeline {
         ensure_staging();
         std::vector<double> mats(12 * (size_t)opt.batch);
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const int nt = (int)std::min<unsigned>(8, hw);
+        const int nt = (int)std::min<unsigned>(copy_threads(), hw);
         // the records are copied out of a read-only mapping of the file
         // (page-cache pages mapped, no per-call kernel copy); pread when the
         // file cannot be mapped
