@@ -402,7 +402,10 @@ def run_ours(args):
                      force_quad=args.quad)
     band, nb, vol = sstep.band, sstep.proj_bytes, sstep.vol
 
-    nbatch = (n + args.batch - 1) // args.batch
+    # kernel launches per step: the staged kernel takes up to 64 projections
+    # per launch, the gather kernel up to min(batch, 32)
+    per_launch = 64 if sstep.staged else min(args.batch, 32)
+    nbatch = (n + per_launch - 1) // per_launch
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
@@ -855,7 +858,9 @@ def config4_entry(c):
                    err, stream, force_quad=args.quad)
     vol = sst.vol
     res["kernel"] = sst.kernel
-    for batch in (16, 32):
+    for batch in (16,):
+        # device-resident: launches of 64 projections on the staged path
+        # (opt.batch sets the pipeline's upload batches, used by the e2e below)
         sst.opt = pkg.Options(batch=batch, mode=c.mode)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
@@ -878,20 +883,20 @@ def config4_entry(c):
             pk.append(ev[0].elapsed_time(ev[1]))
             bp.append(ev[1].elapsed_time(ev[2]))
         ms = statistics.mean(pk) + statistics.mean(bp)
-        nl = (n + batch - 1) // batch
+        nl = (n + 63) // 64 if sst.staged else (n + min(batch, 32) - 1) // min(batch, 32)
         launch_ms = statistics.mean(bp) / nl
         upd = L ** 3 * (n / nl)
         peaks, _ = measured_peaks()
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         nsm = torch.cuda.get_device_properties(dev).multi_processor_count
         frac = upd * OPS_PER_UPDATE / (launch_ms * 1e-3) / (nsm * 128 * sm_max * 1e6)
-        res[f"batch{batch}"] = {"value": round(L ** 3 * n / (ms * 1e-3) / 1e9, 3),
-                                "unit": "GUp/s", "ms_per_step": round(ms, 2),
-                                "prep_ms": round(statistics.mean(pk), 2),
-                                "roofline_frac": round(frac, 4)}
+        res.update({"value": round(L ** 3 * n / (ms * 1e-3) / 1e9, 3),
+                    "unit": "GUp/s", "ms_per_step": round(ms, 2),
+                    "prep_ms": round(statistics.mean(pk), 2),
+                    "projections_per_launch": 64 if sst.staged else min(batch, 32),
+                    "roofline_frac": round(frac, 4)})
     if int(err.item()) != 0:
         res["error_flag"] = int(err.item())
-    res["value"] = res["batch16"]["value"]
     imgs_h = imgs.cpu().pin_memory()
     sst.release()
     del imgs, vol

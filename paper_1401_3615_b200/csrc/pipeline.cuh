@@ -446,18 +446,48 @@ struct Pipeline {
         launch_scan(dst, W, H, (long long)W * H, n, flags, w.d_err, w.compute);
         if (resident && submitted == 0)
             choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
-        w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, dst,
-                                           (long long)W * H, W, H, 0, H, n, mats, flags, plan, opt,
-                                           w.d_err, w.compute, resident ? w.tail_lo : 0,
-                                           resident ? w.tail_hi : 0,
-                                           w.count_culled ? w.d_counters : nullptr);
-        if (!resident)
-            CK(cudaEventRecord(w.raw_free[slot], w.compute));
-        ++nbatch;
-        if (resident)
+        if (resident) {
+            // the stack stays in HBM: back-project in launches of up to
+            // kTmaBatch resident projections (the upload batch only sets the
+            // streaming granularity, e.g. BASELINE config 4's batches of 16);
+            // during the ramp-up (batches below opt.batch) launch at once
             std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
+            // launch sizes keep growing like the upload ramp (4, 4, 8, 16,
+            // 32, 64, 64, ...): never more than twice the previous launch, so
+            // the device is not left waiting for a large accumulation
+            const int pend = (int)(submitted + n) - raw_pending;
+            if (n < opt.batch || pend >= std::min(kTmaBatch, 2 * raw_last_launch))
+                launch_raw_pending((int)(submitted + n));
+        } else {
+            w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, dst,
+                                               (long long)W * H, W, H, 0, H, n, mats, flags, plan,
+                                               opt, w.d_err, w.compute, 0, 0,
+                                               w.count_culled ? w.d_counters : nullptr);
+            CK(cudaEventRecord(w.raw_free[slot], w.compute));
+        }
+        ++nbatch;
         submitted += n;
         slot = (slot + 1) % nslots;
+    }
+
+    // raw resident mode: resident projections [raw_pending, end) not yet
+    // back-projected into the head planes
+    int raw_pending = 0;
+    int raw_last_launch = 0;
+    void launch_raw_pending(int end) {
+        if (end <= raw_pending)
+            return;
+        Worker& w = *workers[0];
+        CK(cudaSetDevice(w.device));
+        const int n = end - raw_pending;
+        raw_last_launch = n;
+        w.guarded += launch_backproject_raw(
+            w.d_vol, g, w.z_begin, w.z_end,
+            static_cast<const float*>(w.d_packed_all) + (size_t)raw_pending * W * H,
+            (long long)W * H, W, H, 0, H, n, all_mats.data() + 12 * (size_t)raw_pending,
+            w.d_flags_all + raw_pending, plan, opt, w.d_err, w.compute, w.tail_lo, w.tail_hi,
+            w.count_culled ? w.d_counters : nullptr);
+        raw_pending = end;
     }
 
     // host time spent issuing batches (CBB_TRACE: printed per call), the
@@ -909,6 +939,8 @@ struct Pipeline {
     void finish(float* vol_out) {
         NvtxRange range("cbb finish");
         flush();
+        if (raw_mode && resident)
+            launch_raw_pending((int)submitted);
         if (std::getenv("CBB_TRACE") && issue_count)
             std::fprintf(stderr,
                          "cbb: %d worker(s), %s mode: %llu batches issued, host issue %.3f ms "
