@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base dem
     python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launch list exit=$?"
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:cbb::bp_(tma_)?kernel' -s 40 -c 1 -o gpurun_out/prof_$TAG -f \
+    -k 'regex:cbb::bp_(tma_)?kernel' -s 20 -c 1 -o gpurun_out/prof_$TAG -f \
     python bench.py $ARGS > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full capture exit=$?"
