@@ -241,3 +241,53 @@ def test_pipeline_raw_mode_guarded_batch_with_resident_tail(scan, oracle, monkey
     st = pkg.reconstruct_arrays(v, g, host, m, pkg.Options(num_gpus=1, batch=8))
     assert st["guarded_batches"] >= 1
     assert bits_equal(v, ref)
+
+
+@pytest.mark.parametrize("kind", ["unaligned_rows", "coarse_voxels"])
+def test_raw_device_entry_falls_back_to_packing(cuda, oracle, kind):
+    """cbb_backproject_raw_device when the staged kernel cannot run -- rows
+    not 16-byte aligned (W % 4 != 0) or footprint boxes over the budget
+    (coarse voxels): it packs internally and runs the gather kernel, same
+    bits as the reference."""
+    import torch
+
+    if kind == "unaligned_rows":
+        cfg = synth.shrunk(synth.CONFIGS[2], edge_voxels=48, num_projections=12, width=1247,
+                           height=960)
+        g = VolumeGeometry.centered(48, 0.5)
+    else:
+        cfg = synth.shrunk(synth.CONFIGS[0], edge_voxels=48, num_projections=12)
+        g = cfg.geometry
+    _, mats, imgs = synth.make_inputs(cfg, device="cuda", chunk=12)
+    n, H, W = imgs.shape
+    assert pkg.tma_plan(g, W, H, 0, 48, mats)["staged"] == 0
+    ref = np.zeros((48,) * 3, np.float32)
+    assert oracle.reconstruct(ref, g, imgs.cpu().numpy(), mats) == 0
+    flags = torch.zeros(n, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pkg.scan_device(imgs, flags, err)
+    v = torch.zeros((48, 48, 48), dtype=torch.float32, device="cuda")
+    pkg.backproject_raw_device(v, g, 0, 48, imgs, W, H, n, mats, flags, pkg.Options(), err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0 and bits_equal(v.cpu().numpy(), ref)
+
+
+def test_scan_flags_and_nonfinite(cuda):
+    """scan_projections: bit 0 of a projection's flag when a pixel reaches
+    2^86 (the exact division's numerator bound), err bit 2 on a non-finite
+    pixel; unaligned sizes take the scalar loop."""
+    import torch
+
+    for w in (64, 63):
+        x = torch.ones((4, 17, w), dtype=torch.float32, device="cuda")
+        x[1, 3, 5] = 2.0 ** 86
+        x[2, 16, w - 1] = -(2.0 ** 90)
+        flags = torch.full((4,), 7, dtype=torch.int32, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        pkg.scan_device(x, flags, err)
+        torch.cuda.synchronize()
+        assert flags.tolist() == [0, 1, 1, 0] and int(err.item()) == 0
+        x[3, 0, 0] = float("inf")
+        pkg.scan_device(x, flags, err)
+        torch.cuda.synchronize()
+        assert int(err.item()) & 2
