@@ -551,7 +551,8 @@ cbb_status cbb_backproject_raw_device(float* vol_slab, const cbb_volume_geometry
         if (std::getenv("CBB_TRACE"))
             std::fprintf(stderr, "cbb: tma plan ok %d pitch %d bh %d stages %d (need %d x %d)\n", plan.ok,
                          plan.pitch, plan.bh, plan.stages, plan.bw_need, plan.bh_need);
-        if (plan.ok && tma_path_enabled() && (uintptr_t)raw % 16 == 0 && raw_stride % 4 == 0) {
+        if (plan.ok && tma_path_enabled() && (uintptr_t)raw % 16 == 0 && raw_stride % 4 == 0 &&
+            b.rn >= 1) {
             launch_backproject_raw(vol_slab, *geometry, z_begin, z_end, raw, raw_stride, width,
                                    height, b.r0, b.rn, count, mats, flags, plan, opt, err_flag,
                                    st);

@@ -55,6 +55,7 @@ struct Worker {
     // current batch, or of every resident projection
     unsigned* d_flags = nullptr;
     unsigned* d_flags_all = nullptr;
+    TmaPlan plan;                      // this slab's staging plan (raw mode)
 
     ~Worker() {
         if (!copy)
@@ -188,7 +189,6 @@ struct Pipeline {
     // projections by the TMA-staged kernel -- no packing, and resident mode
     // keeps the raw stack (4.8x smaller than the packed one).
     bool raw_mode = false;
-    TmaPlan plan;
     int tail_group() const { return raw_mode ? kTR : 8; }
 
     // Resident mode for a stack of known size: when every packed projection
@@ -419,6 +419,8 @@ struct Pipeline {
     // issue() in raw mode (one worker): upload (into the resident raw stack
     // or a ring slot), optional ramp filter, scan, TMA back-projection.
     void issue_raw(const float* src, const double* mats, int n, int stage) {
+        if (workers.size() > 1)
+            return issue_raw_multi(src, mats, n, stage);
         NvtxRange range("cbb batch (raw)");
         Worker& w = *workers[0];
         CK(cudaSetDevice(w.device));
@@ -460,12 +462,104 @@ struct Pipeline {
                 launch_raw_pending((int)(submitted + n));
         } else {
             w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, dst,
-                                               (long long)W * H, W, H, 0, H, n, mats, flags, plan,
-                                               opt, w.d_err, w.compute, 0, 0,
+                                               (long long)W * H, W, H, 0, H, n, mats, flags,
+                                               w.plan, opt, w.d_err, w.compute, 0, 0,
                                                w.count_culled ? w.d_counters : nullptr);
             CK(cudaEventRecord(w.raw_free[slot], w.compute));
         }
         ++nbatch;
+        submitted += n;
+        slot = (slot + 1) % nslots;
+    }
+
+    // issue_raw with several workers: batch k is uploaded once by worker
+    // k mod G; every worker holds its slab's band of raw rows -- the root
+    // copies its band out of its slot (into its resident stack) or reads it in
+    // place, the others copy theirs from the root's slot peer-to-peer (the
+    // staged kernel reads local memory through its tensor map); each then
+    // scans its rows and runs the TMA-staged kernel on them.
+    void issue_raw_multi(const float* src, const double* mats, int n, int stage) {
+        NvtxRange range("cbb batch (raw, multi)");
+        const int G = (int)workers.size();
+        Worker& root = *workers[nbatch % G];
+        // slot reuse, as in issue_packed: the root's slot is read by its own
+        // kernels (raw_free) and the other workers' band copies (h2d_done);
+        // a non-root worker's slot is rewritten by its next band copy
+        CK(cudaSetDevice(root.device));
+        for (auto& o : workers) {
+            CK(cudaStreamWaitEvent(root.copy, o->raw_free[slot], 0));
+            if (o.get() != &root)
+                CK(cudaStreamWaitEvent(root.copy, o->h2d_done[slot], 0));
+        }
+        for (auto& w : workers)
+            if (w.get() != &root) {
+                CK(cudaSetDevice(w->device));
+                CK(cudaStreamWaitEvent(w->copy, w->raw_free[slot], 0));
+            }
+        CK(cudaSetDevice(root.device));
+        CK(cudaMemcpyAsync(root.d_raw[slot], src, raw_bytes_per_proj * n, cudaMemcpyHostToDevice,
+                           root.copy));
+        CK(cudaEventRecord(root.h2d_done[slot], root.copy));
+        if (stage >= 0) {
+            CK(cudaEventRecord(root.stage_read[stage], root.copy));
+            stage_owner[stage] = (int)(nbatch % G);
+        }
+        CK(cudaStreamWaitEvent(root.compute, root.h2d_done[slot], 0));
+        start_timing(root);
+        cudaEvent_t ready = root.h2d_done[slot];
+        if (opt.ramp_filter) {
+            ramp_filter_device(root.d_raw[slot], root.d_raw[slot], W, H, n, opt.filter_pixel_mm,
+                               root.compute);
+            CK(cudaEventRecord(root.src_ready[slot], root.compute));
+            ready = root.src_ready[slot];
+        }
+        // the root sees the whole batch: it checks the pixels no band holds
+        if (!root.band.is_full(H))
+            launch_check_finite(root.d_raw[slot], (long long)n * W * H, root.d_err, root.compute);
+        if (resident && submitted == 0)
+            choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
+        for (auto& wp : workers) {
+            Worker& w = *wp;
+            CK(cudaSetDevice(w.device));
+            const int r0 = w.band.r0, rows = w.band.rn;
+            const size_t band_bytes = (size_t)rows * W * sizeof(float);
+            float* res = resident ? static_cast<float*>(w.d_packed_all) + (size_t)submitted * rows * W
+                                  : nullptr;
+            unsigned* flags = resident ? w.d_flags_all + submitted : w.d_flags;
+            const float* rows_ptr;
+            long long stride;
+            if (&w == &root) {
+                if (resident) {
+                    CK(cudaMemcpy2DAsync(res, band_bytes, root.d_raw[slot] + (size_t)r0 * W,
+                                         raw_bytes_per_proj, band_bytes, n,
+                                         cudaMemcpyDeviceToDevice, w.compute));
+                    rows_ptr = res;
+                    stride = (long long)rows * W;
+                } else {
+                    rows_ptr = root.d_raw[slot] + (size_t)r0 * W;
+                    stride = (long long)W * H;
+                }
+            } else {
+                float* d = resident ? res : w.d_raw[slot];
+                CK(cudaStreamWaitEvent(w.copy, ready, 0));
+                copy_band_to(root, w, slot, n, d);
+                CK(cudaEventRecord(w.h2d_done[slot], w.copy));
+                CK(cudaStreamWaitEvent(w.compute, w.h2d_done[slot], 0));
+                start_timing(w);
+                rows_ptr = d;
+                stride = (long long)rows * W;
+            }
+            launch_scan(rows_ptr, W, rows, stride, n, flags, w.d_err, w.compute);
+            w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, rows_ptr, stride,
+                                               W, H, r0, rows, n, mats, flags, w.plan, opt,
+                                               w.d_err, w.compute, resident ? w.tail_lo : 0,
+                                               resident ? w.tail_hi : 0,
+                                               w.count_culled ? w.d_counters : nullptr);
+            CK(cudaEventRecord(w.raw_free[slot], w.compute));
+        }
+        ++nbatch;
+        if (resident)
+            std::memcpy(all_mats.data() + 12 * submitted, mats, 12 * sizeof(double) * n);
         submitted += n;
         slot = (slot + 1) % nslots;
     }
@@ -485,7 +579,7 @@ struct Pipeline {
             w.d_vol, g, w.z_begin, w.z_end,
             static_cast<const float*>(w.d_packed_all) + (size_t)raw_pending * W * H,
             (long long)W * H, W, H, 0, H, n, all_mats.data() + 12 * (size_t)raw_pending,
-            w.d_flags_all + raw_pending, plan, opt, w.d_err, w.compute, w.tail_lo, w.tail_hi,
+            w.d_flags_all + raw_pending, w.plan, opt, w.d_err, w.compute, w.tail_lo, w.tail_hi,
             w.count_culled ? w.d_counters : nullptr);
         raw_pending = end;
     }
@@ -619,7 +713,8 @@ struct Pipeline {
     // Rows [band.r0, band.r0 + band.rn) of the batch's n projections, from the
     // root's full raw slot to w's band slot (projection stride rn * W), one
     // strided peer copy on w's copy stream.
-    void copy_band(const Worker& root, Worker& w, int s, int n) {
+    void copy_band(const Worker& root, Worker& w, int s, int n) { copy_band_to(root, w, s, n, w.d_raw[s]); }
+    void copy_band_to(const Worker& root, Worker& w, int s, int n, float* dst) {
         const RowBand& b = w.band;
         if (b.rn <= 0)
             return;
@@ -628,7 +723,7 @@ struct Pipeline {
         p.srcPtr = make_cudaPitchedPtr(root.d_raw[s] + (size_t)b.r0 * W, raw_bytes_per_proj,
                                        row_bytes, n);
         p.srcDevice = root.device;
-        p.dstPtr = make_cudaPitchedPtr(w.d_raw[s], row_bytes, row_bytes, n);
+        p.dstPtr = make_cudaPitchedPtr(dst, row_bytes, row_bytes, n);
         p.dstDevice = w.device;
         p.extent = make_cudaExtent(row_bytes, n, 1);
         CK(cudaMemcpy3DPeerAsync(&p, w.copy));
@@ -736,27 +831,44 @@ struct Pipeline {
         NvtxRange range("cbb setup (bands, resident)");
         const auto t0 = std::chrono::steady_clock::now();
         set_bands(mats, count);
-        if (workers.size() == 1 && tma_path_enabled()) {
-            Worker& w = *workers[0];
-            plan = plan_tma(g, W, H, w.z_begin, w.z_end, mats, count);
-            raw_mode = plan.ok;
+        if (tma_path_enabled()) {
+            raw_mode = true;
+            for (auto& w : workers) {
+                w->plan = plan_tma(g, W, H, w->z_begin, w->z_end, mats, count);
+                raw_mode = raw_mode && w->plan.ok;
+            }
             if (raw_mode) {
-                w.band = RowBand::full(H);
-                w.pk_bytes = raw_bytes_per_proj; // resident stack: raw projections
-                CK(cudaSetDevice(w.device));
-                w.d_flags = static_cast<unsigned*>(
-                    DevicePool::get().alloc(w.device, sizeof(unsigned) * opt.batch));
+                for (auto& w : workers) {
+                    // one device: the whole detector (uploads land in place);
+                    // several: each keeps its slab's band of raw rows
+                    if (workers.size() == 1)
+                        w->band = RowBand::full(H);
+                    if (w->band.rn < 1) { // footprint off the detector: hold one row
+                        // (a tensor map needs >= 1 row; extra rows hold true pixels)
+                        w->band.r0 = std::min(std::max(w->band.r0, 0), H - 1);
+                        w->band.rn = 1;
+                    }
+                    w->pk_bytes = (size_t)w->band.rn * W * sizeof(float); // resident rows
+                    CK(cudaSetDevice(w->device));
+                    w->d_flags = static_cast<unsigned*>(
+                        DevicePool::get().alloc(w->device, sizeof(unsigned) * opt.batch));
+                }
             }
             if (std::getenv("CBB_TRACE"))
-                std::fprintf(stderr, "cbb: raw mode %d (tma pitch %d bh %d stages %d)\n",
-                             (int)raw_mode, plan.pitch, plan.bh, plan.stages);
+                for (auto& w : workers)
+                    std::fprintf(stderr,
+                                 "cbb: raw mode %d, device %d slab [%d, %d): tma pitch %d bh %d "
+                                 "stages %d, rows [%d, %d)\n",
+                                 (int)raw_mode, w->device, w->z_begin, w->z_end, w->plan.pitch,
+                                 w->plan.bh, w->plan.stages, w->band.r0, w->band.r0 + w->band.rn);
         }
         enable_resident(count);
-        if (raw_mode && resident) {
-            Worker& w = *workers[0];
-            w.d_flags_all = static_cast<unsigned*>(
-                DevicePool::get().alloc(w.device, sizeof(unsigned) * count));
-        }
+        if (raw_mode && resident)
+            for (auto& w : workers) {
+                CK(cudaSetDevice(w->device));
+                w->d_flags_all = static_cast<unsigned*>(
+                    DevicePool::get().alloc(w->device, sizeof(unsigned) * count));
+            }
         if (std::getenv("CBB_TRACE"))
             std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
                          std::chrono::duration<double, std::milli>(
@@ -939,7 +1051,7 @@ struct Pipeline {
     void finish(float* vol_out) {
         NvtxRange range("cbb finish");
         flush();
-        if (raw_mode && resident)
+        if (raw_mode && resident && workers.size() == 1)
             launch_raw_pending((int)submitted);
         if (std::getenv("CBB_TRACE") && issue_count)
             std::fprintf(stderr,
@@ -1017,9 +1129,9 @@ struct Pipeline {
                     w->guarded += launch_backproject_raw(
                         w->d_vol + plane * (part.first - w->z_begin), g, part.first,
                         part.second, static_cast<const float*>(w->d_packed_all),
-                        (long long)W * H, W, H, 0, H, resident_count, all_mats.data(),
-                        w->d_flags_all, plan, opt, w->d_err, w->compute, 0, 0,
-                        w->count_culled ? w->d_counters : nullptr);
+                        (long long)w->band.rn * W, W, H, w->band.r0, w->band.rn, resident_count,
+                        all_mats.data(), w->d_flags_all, w->plan, opt, w->d_err, w->compute, 0,
+                        0, w->count_culled ? w->d_counters : nullptr);
                 else if (part.second > part.first)
                     w->guarded += launch_backproject(
                         w->d_vol + plane * (part.first - w->z_begin), g, part.first,

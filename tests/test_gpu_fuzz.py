@@ -128,7 +128,8 @@ def raw_case(seed):
     vol0 = (r.standard_normal((L, L, L)) * float(r.choice([0.0, 1.0]))).astype(np.float32)
     if r.random() < 0.3:
         vol0[r.random(vol0.shape) < 0.1] = -0.0
-    opts = dict(batch=int(r.integers(1, 33)), num_gpus=1, cull=bool(r.random() < 0.85),
+    k = int(r.choice([1, 1, 2, 3]))  # slab workers on the one GPU
+    opts = dict(batch=int(r.integers(1, 65)), device_ids=[0] * k, cull=bool(r.random() < 0.85),
                 ramp_filter_pixel_mm=None)
     return g, mats, imgs, vol0, opts, r
 
@@ -136,8 +137,10 @@ def raw_case(seed):
 @pytest.mark.parametrize("seed", range(int(os.environ.get("CBB_FUZZ_RAW_SEEDS", "48"))))
 def test_fuzz_raw_mode_vs_oracle(cuda, oracle, monkeypatch, seed):
     """The staged (raw-mode) pipeline on random scans, bitwise against the
-    oracle: resident tail on/off, forced small boxes (global-memory taps) in a
-    third of the cases, contiguous / per-image / pageable inputs."""
+    oracle: 1-3 slab workers (band rows copied from the uploading worker),
+    upload batches 1-64, resident tail on/off, forced small boxes
+    (global-memory taps) in a third of the cases, contiguous / per-image /
+    pageable inputs."""
     g, mats, imgs, vol0, opts, r = raw_case(seed)
     n, H, W = imgs.shape
     if r.random() < 0.33:

@@ -291,3 +291,23 @@ def test_scan_flags_and_nonfinite(cuda):
         pkg.scan_device(x, flags, err)
         torch.cuda.synchronize()
         assert int(err.item()) & 2
+
+
+@pytest.mark.parametrize("resident", [True, False])
+def test_pipeline_raw_mode_several_workers(scan, expected, monkeypatch, resident):
+    """Raw mode with 3 slab workers on the one GPU: each keeps its band of
+    raw rows (the uploading worker copies its band out of its slot, the others
+    copy theirs from it), scans and back-projects them -- bitwise; with a
+    forced guarded batch too."""
+    g, mats, imgs = scan
+    if not resident:
+        monkeypatch.setenv("CBB_NO_RESIDENT", "1")
+    host = imgs.cpu().numpy()
+    v = np.zeros((L, L, L), np.float32)
+    st = pkg.reconstruct_arrays(v, g, host, mats, pkg.Options(device_ids=[0, 0, 0], batch=8))
+    assert st["num_gpus"] == 3
+    assert bits_equal(v, expected)
+    monkeypatch.setenv("CBB_FORCE_GUARDED", "1")
+    v = np.zeros((L, L, L), np.float32)
+    st = pkg.reconstruct_arrays(v, g, host, mats, pkg.Options(device_ids=[0, 0], batch=16))
+    assert st["guarded_batches"] > 0 and bits_equal(v, expected)
