@@ -38,6 +38,11 @@ constexpr int kTBX = 16, kTBY = 16;   // block tile in x, y (voxels)
 #define CBB_TMA_R 12
 #endif
 constexpr int kTR = CBB_TMA_R;        // voxels per thread along z
+// Voxel-pair body (bp_project_p): every per-voxel quantity of two z-neighbours
+// in one f32x2 register, taps included; 0 = bp_project_f (pairs within a voxel).
+#ifndef CBB_TMA_PAIRS
+#define CBB_TMA_PAIRS 1
+#endif
 // guarded kernel: voxels per thread along z -- the same z-blocks as the staged
 // kernel, so a resident tail gap (aligned to kTR) maps identically
 constexpr int kGR = kTR;
@@ -77,7 +82,7 @@ struct TmaMats {
 template <int R>
 __device__ BlockTables<R> tma_block_setup(const TmaArgs& args, const TmaMats& mats, int zoff) {
     __shared__ float s_m[kTmaBatch * 12];
-    __shared__ f2 s_zuv[kTmaBatch * R];
+    __shared__ __align__(16) f2 s_zuv[kTmaBatch * R];
     __shared__ f2 s_zw[kTmaBatch * (R / 2)];
     const float* flat = &mats.a[0][0];
     for (int i = threadIdx.x; i < args.count * 12; i += blockDim.x)
@@ -86,8 +91,16 @@ __device__ BlockTables<R> tma_block_setup(const TmaArgs& args, const TmaMats& ma
     for (int i = threadIdx.x; i < args.count * R; i += blockDim.x) {
         const int p = i / R, r = i % R;
         const float* a = flat + 12 * p;
+#if CBB_TMA_PAIRS
+        // voxel pairs: entry 2k + c = (wz_2k * a[6 + c], wz_2k+1 * a[6 + c])
+        const int k = r / 2, c = r % 2;
+        const float wz0 = __fadd_rn(args.O, __fmul_rn((float)min(z0 + 2 * k, zl), args.MM));
+        const float wz1 = __fadd_rn(args.O, __fmul_rn((float)min(z0 + 2 * k + 1, zl), args.MM));
+        s_zuv[i] = pk(__fmul_rn(wz0, a[M67 + c]), __fmul_rn(wz1, a[M67 + c]));
+#else
         const float wz = __fadd_rn(args.O, __fmul_rn((float)min(z0 + r, zl), args.MM));
         s_zuv[i] = pk(__fmul_rn(wz, a[M67]), __fmul_rn(wz, a[M67 + 1]));
+#endif
     }
     for (int i = threadIdx.x; i < args.count * (R / 2); i += blockDim.x) {
         const int p = i / (R / 2), k = i % (R / 2);
@@ -205,6 +218,29 @@ struct SmemFetch {
         asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(tr) : "r"(a), "n"(PITCH * 4 + 4));
         return make_float4(bl, tl, br, tr);
     }
+    // Taps of two voxels as pairs (bl0, bl1), (tl0, tl1), ... : the cell
+    // indices of both in one FADD2 + FFMA2 (integer-valued, exact).
+    __device__ __forceinline__ void pair(f2 ixt, f2 iyt, f2& bl, f2& tl, f2& br, f2& tr) const {
+        const f2 idx = fma2(iyt, bc((float)PITCH), add2(ixt, bc(bias)));
+        float i0, i1;
+        upk(idx, i0, i1);
+        unsigned a0, a1;
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a0) : "r"(__float_as_int(i0)), "r"(sbase));
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a1) : "r"(__float_as_int(i1)), "r"(sbase));
+        float b0, b1, r0, r1, t0, t1, q0, q1;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(b0) : "r"(a0));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(b1) : "r"(a1));
+        asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(r0) : "r"(a0));
+        asm volatile("ld.shared.f32 %0, [%1+4];" : "=f"(r1) : "r"(a1));
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(t0) : "r"(a0), "n"(PITCH * 4));
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(t1) : "r"(a1), "n"(PITCH * 4));
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(q0) : "r"(a0), "n"(PITCH * 4 + 4));
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(q1) : "r"(a1), "n"(PITCH * 4 + 4));
+        bl = pk(b0, b1);
+        br = pk(r0, r1);
+        tl = pk(t0, t1);
+        tr = pk(q0, q1);
+    }
 };
 
 // From the raw projection in global memory with the reference's per-tap
@@ -221,7 +257,22 @@ struct RawFetch {
         const int x = (int)ixt, y = (int)iyt;
         return make_float4(tap(x, y), tap(x, y + 1), tap(x + 1, y), tap(x + 1, y + 1));
     }
+    __device__ __forceinline__ void pair(f2 ixt, f2 iyt, f2& bl, f2& tl, f2& br, f2& tr) const {
+        float x0, x1, y0, y1;
+        upk(ixt, x0, x1);
+        upk(iyt, y0, y1);
+        const float4 a = (*this)(x0, y0), b = (*this)(x1, y1);
+        bl = pk(a.x, b.x);
+        tl = pk(a.y, b.y);
+        br = pk(a.z, b.z);
+        tr = pk(a.w, b.w);
+    }
 };
+
+// exact mode: 1/(w*w) from RN(y*y) instead of a second MUFU.RCP (below)
+#ifndef CBB_TMA_YY
+#define CBB_TMA_YY 1
+#endif
 
 // bp_project (bp_kernels.cuh) with the taps from `fetch` (no clamping: the
 // fetcher covers every tap position of the tile). Operation for operation
@@ -321,6 +372,93 @@ __device__ __forceinline__ void bp_project_f(const TmaArgs& args, const float* m
     }
 }
 
+// bp_project_f with voxel pairs in the lanes: (u0, u1), (v0, v1), (ix0, ix1),
+// ..., the taps (bl0, bl1), ... and the two lerps, so the y-lerp and the tap
+// addresses pack too (~3 instructions fewer per voxel). Same operations on
+// the same operands as bp_project_f, so the same bits. zuv: the pair layout
+// of tma_block_setup (CBB_TMA_PAIRS).
+template <int R, int MODE, class Fetch>
+__device__ __forceinline__ void bp_project_p(const TmaArgs& args, const float* m, float wx,
+                                             float wy, const f2* zuv, const f2* zw,
+                                             f2 (&accp)[R / 2], unsigned& vmin,
+                                             const Fetch& fetch) {
+    const f2 NZ = args.neg_zero2;
+    const f2 ONE2 = bc(1.0f);
+    const f2 ZERO2 = bc(0.0f);
+    const f2 tuv = add2(MUL2(ld2(m, M01), bc(wx)), MUL2(ld2(m, M34), bc(wy)));
+    float tu, tv;
+    upk(tuv, tu, tv);
+    const float tw = __fadd_rn(__fmul_rn(wx, m[M2]), __fmul_rn(wy, m[M5]));
+#ifdef CBB_TMA_GP
+    constexpr int GP = CBB_TMA_GP;         // voxel pairs in flight (tuning hook)
+#else
+    constexpr int GP = R % 4 == 0 ? 2 : 1; // voxel pairs in flight
+#endif
+    static_assert((R / 2) % GP == 0, "pairs per group");
+#pragma unroll
+    for (int g = 0; g < R / (2 * GP); ++g) {
+        f2 wpair[GP], ypair[GP], sx[GP], sy[GP], bl[GP], tl[GP], br[GP], tr[GP];
+#pragma unroll
+        for (int k = 0; k < GP; ++k) {
+            const int kk = g * GP + k;
+            const f2 w01 = add2(add2(bc(tw), zw[kk]), bc(m[M11]));
+            wpair[k] = w01;
+            float w0, w1;
+            upk(w01, w0, w1);
+            const f2 r01 = pk(rcp_approx(w0), rcp_approx(w1));
+            const f2 y01 = fma2(r01, fma2(neg2(w01), r01, ONE2), r01);
+            ypair[k] = y01;
+            const float4 z4 = *reinterpret_cast<const float4*>(zuv + 2 * kk);
+            const f2 u01 = add2(add2(bc(tu), pk(z4.x, z4.y)), bc(m[M910]));
+            const f2 v01 = add2(add2(bc(tv), pk(z4.z, z4.w)), bc(m[M910 + 1]));
+            const f2 qu = fma2(u01, y01, ZERO2);
+            const f2 ix01 = fma2(y01, fma2(neg2(w01), qu, u01), qu);
+            const f2 qv = fma2(v01, y01, ZERO2);
+            const f2 iy01 = fma2(y01, fma2(neg2(w01), qv, v01), qv);
+            float ix0, ix1, iy0, iy1;
+            upk(ix01, ix0, ix1);
+            upk(iy01, iy0, iy1);
+            const f2 ixt = pk(truncf(ix0), truncf(ix1));
+            const f2 iyt = pk(truncf(iy0), truncf(iy1));
+            sx[k] = add2(ix01, neg2(ixt));
+            sy[k] = add2(iy01, neg2(iyt));
+            fetch.pair(ixt, iyt, bl[k], tl[k], br[k], tr[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < GP; ++k) {
+            const f2 omsx = add2(ONE2, neg2(sx[k]));
+            const f2 omsy = add2(ONE2, neg2(sy[k]));
+            const f2 vb = add2(MUL2(bl[k], omsx), MUL2(br[k], sx[k]));
+            const f2 vt = add2(MUL2(tl[k], omsx), MUL2(tr[k], sx[k]));
+            const f2 vv = add2(MUL2(omsy, vb), MUL2(sy[k], vt));
+            f2 c;
+            if (MODE == 0) {
+                const f2 ww = MUL2(wpair[k], wpair[k]);
+#if CBB_TMA_YY
+                const f2 r2 = MUL2(ypair[k], ypair[k]);
+#else
+                float ww0, ww1;
+                upk(ww, ww0, ww1);
+                const f2 r2 = pk(rcp_approx(ww0), rcp_approx(ww1));
+#endif
+                const f2 y2 = fma2(r2, fma2(neg2(ww), r2, ONE2), r2);
+                const f2 q0 = MUL2(vv, y2);
+                c = fma2(neg2(y2), fma2(ww, q0, neg2(vv)), q0);
+                float val[2];
+                upk(vv, val[0], val[1]);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned e = __float_as_uint(val[h]) << 1;
+                    vmin = min(vmin, e - 1u);
+                }
+            } else {
+                c = MUL2(vv, MUL2(ypair[k], ypair[k]));
+            }
+            accp[g * GP + k] = add2(accp[g * GP + k], c);
+        }
+    }
+}
+
 // update_ieee (bp_kernels.cuh) with raw taps: IEEE divisions, optional
 // reference guards.
 template <int MODE, bool GUARD>
@@ -377,11 +515,13 @@ __device__ __forceinline__ void corner_extent(const float* a, const float cx[2],
 // threads, dynamic shared memory: S stages of PITCH * bh floats, then 2 S
 // mbarriers.
 // ---------------------------------------------------------------------------
-#ifndef CBB_TMA_YY
-#define CBB_TMA_YY 1
-#endif
 #ifndef CBB_TMA_MINB
 #define CBB_TMA_MINB 3
+#endif
+#if CBB_TMA_PAIRS
+#define CBB_TMA_BODY bp_project_p
+#else
+#define CBB_TMA_BODY bp_project_f
 #endif
 template <int MODE, int PITCH, bool CNT>
 __global__ void __launch_bounds__(kTThreads, CBB_TMA_MINB)
@@ -562,7 +702,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         mbar_wait_a(full0 + 8u * (unsigned)cslot, cph);
         if ((todo >> p) & 1ull) {
             const SmemFetch<PITCH> f{sbc, s_bias[p]};
-            bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
+            CBB_TMA_BODY<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
                                   tabs.zw + p * (R / 2), accp, vmin, f);
         }
         __syncwarp();
@@ -596,7 +736,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             if ((tma_mask >> p) & 1ull)
                 staged(p);
             else if ((todo >> p) & 1ull)
-                bp_project_f<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
+                CBB_TMA_BODY<R, MODE>(args, mats.a[p], wx, wy, tabs.zuv + p * R,
                                       tabs.zw + p * (R / 2), accp, vmin, raw_fetch(args, p));
         }
     }
