@@ -160,6 +160,30 @@ def test_negative_zero_voxels_and_culling(scan, oracle):
         assert err == 0 and bits_equal(v, ref)
 
 
+def test_negative_zero_voxels_off_centre(scan, oracle):
+    """-0.0 voxels where culling does skip work (an off-centre cube past the
+    detector edge): exact mode recomputes their threads with IEEE divisions
+    (bitwise the oracle); fast mode switches culling off for their warps
+    (culling on = culling off, bitwise)."""
+    g0, mats, imgs = scan
+    g = VolumeGeometry(L, g0.voxel_mm, 60.0)
+    host = imgs.cpu().numpy()
+    n, H, W = host.shape
+    assert pkg.tma_plan(g, W, H, 0, L, mats)["staged"] == 1
+    r = np.random.default_rng(7)
+    vol0 = np.zeros((L, L, L), np.float32)
+    vol0[r.random(vol0.shape) < 0.05] = -0.0
+    vol0[:, :8, :] = -0.0
+    vol0[::9, ::4, ::5] = 0.25
+    ref = vol0.copy()
+    assert oracle.reconstruct(ref, g, host, mats) == 0
+    v, err = raw_device(g, mats, imgs, vol0=vol0)
+    assert err == 0 and bits_equal(v, ref)
+    fast = [raw_device(g, mats, imgs, vol0=vol0, mode=pkg.MODE_FAST, cull=c)[0]
+            for c in (True, False)]
+    assert bits_equal(fast[0], fast[1])
+
+
 @pytest.mark.parametrize("resident", [True, False])
 def test_pipeline_raw_mode(scan, expected, monkeypatch, resident):
     """cbb_reconstruct on one GPU with the whole stack known runs in raw mode
