@@ -337,7 +337,15 @@ struct Pipeline {
             w->z_end = bounds.empty() ? s0 + (int)((long long)(s1 - s0) * (i + 1) / ng)
                                       : bounds[i + 1];
             CK(cudaSetDevice(w->device));
-            CK(cudaStreamCreateWithFlags(&w->copy, cudaStreamNonBlocking));
+            {
+                // the copy stream also runs the resident scan (issue_raw): high
+                // priority, so its blocks take the first SM slots the
+                // back-projection frees instead of waiting for the launch to drain
+                int lo = 0, hi = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CK(cudaStreamCreateWithPriority(&w->copy, cudaStreamNonBlocking,
+                                                std::getenv("CBB_COPY_PRIO0") ? lo : hi));
+            }
             CK(cudaStreamCreateWithFlags(&w->compute, cudaStreamNonBlocking));
             nslots = std::min(kMaxSlots, std::max(2, ng + 1));
             for (int s = 0; s < nslots; ++s) {
@@ -436,16 +444,25 @@ struct Pipeline {
             CK(cudaStreamWaitEvent(w.copy, w.raw_free[slot], 0));
         }
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, w.copy));
-        CK(cudaEventRecord(w.h2d_done[slot], w.copy));
         if (stage >= 0) {
             CK(cudaEventRecord(w.stage_read[stage], w.copy));
             stage_owner[stage] = 0;
         }
+        // resident, pre-filtered stack: scan right behind the upload on the
+        // (high-priority) copy stream -- per-projection flags, nothing else
+        // reads them yet -- so it overlaps the back-projection instead of
+        // queueing between launches (at default priority its blocks waited
+        // for each launch to drain and stalled the uploads: 95 vs 78 ms)
+        const bool scan_on_copy = resident && !opt.ramp_filter && !std::getenv("CBB_SCAN_COMPUTE");
+        if (scan_on_copy)
+            launch_scan(dst, W, H, (long long)W * H, n, flags, w.d_err, w.copy);
+        CK(cudaEventRecord(w.h2d_done[slot], w.copy));
         CK(cudaStreamWaitEvent(w.compute, w.h2d_done[slot], 0));
         start_timing(w);
         if (opt.ramp_filter)
             ramp_filter_device(dst, dst, W, H, n, opt.filter_pixel_mm, w.compute);
-        launch_scan(dst, W, H, (long long)W * H, n, flags, w.d_err, w.compute);
+        if (!scan_on_copy)
+            launch_scan(dst, W, H, (long long)W * H, n, flags, w.d_err, w.compute);
         if (resident && submitted == 0)
             choose_tails(est_mats ? est_mats : mats, est_mats ? est_n : n);
         if (resident) {
@@ -458,7 +475,17 @@ struct Pipeline {
             // 32, 64, 64, ...): never more than twice the previous launch, so
             // the device is not left waiting for a large accumulation
             const int pend = (int)(submitted + n) - raw_pending;
-            if (n < opt.batch || pend >= std::min(kTmaBatch, 2 * raw_last_launch))
+            // and with the upload ramp on (small slabs), every batch of the
+            // first 128 projections is launched at once too: accumulating to
+            // 2x the last launch there left the device waiting for uploads
+            // (config 2 end to end 78.1 -> 76.5 ms; CBB_LAUNCH_RAMP: experiments)
+            static const int launch_ramp_env = std::getenv("CBB_LAUNCH_RAMP")
+                                                   ? std::atoi(std::getenv("CBB_LAUNCH_RAMP"))
+                                                   : -1;
+            const int launch_ramp = launch_ramp_env >= 0 ? launch_ramp_env
+                                                         : (ramp_ < opt.batch ? 128 : 0);
+            if (n < opt.batch || (int)(submitted + n) <= launch_ramp ||
+                pend >= std::min(kTmaBatch, 2 * raw_last_launch))
                 launch_raw_pending((int)(submitted + n));
         } else {
             w.guarded += launch_backproject_raw(w.d_vol, g, w.z_begin, w.z_end, dst,
