@@ -10,6 +10,7 @@ import subprocess
 import sys
 
 rep, workload, mode = sys.argv[1], sys.argv[2], sys.argv[3]
+extra = dict(a.split("=", 1) for a in sys.argv[4:])  # e.g. projections_per_launch=64
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
                      check=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -21,7 +22,10 @@ for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
     tot += float(v) * scale[u]
 path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json")
 data = json.load(open(path)) if os.path.exists(path) else {}
-data[f"{workload}/{mode}"] = {"dram_bytes_per_launch": tot, "kernel": d.get("Kernel Name", ("", ""))[1],
-                              "source": os.path.basename(rep)}
+kname = d.get("Kernel Name", ("", ""))[1]
+short = kname.split("(")[0].split("<")[0].split()[-1].split("::")[-1]
+entry = {"dram_bytes_per_launch": tot, "kernel": kname, "source": os.path.basename(rep)}
+entry.update({k: int(v) if v.isdigit() else v for k, v in extra.items()})
+data[f"{workload}/{mode}/{short}"] = entry
 json.dump(data, open(path, "w"), indent=1)
 print(data)
