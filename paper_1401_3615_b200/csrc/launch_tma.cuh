@@ -52,7 +52,10 @@ inline CUtensorMap raw_tensor_map(const float* raw, int W, int rows, long long s
 // Box widths the kernel is instantiated for (== 16 mod 32 floats: the rows
 // iy and iy + 1 of a warp's taps fall on shifted bank halves).
 constexpr int kPitches[] = {48, 80, 112, 144};
-constexpr int kTmaSmemBudget = 60 * 1024; // stages per block: 3 blocks/SM (+13.5 KB static)
+#ifndef CBB_TMA_SMEM_KB
+#define CBB_TMA_SMEM_KB 60
+#endif
+constexpr int kTmaSmemBudget = CBB_TMA_SMEM_KB * 1024; // stages per block: 3 blocks/SM (+13.5 KB static)
 constexpr int kTmaMinStages = 3;
 
 struct TmaPlan {
