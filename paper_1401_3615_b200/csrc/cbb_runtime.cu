@@ -15,11 +15,13 @@
 // downloaded into the caller's volume at the end (no reduction: voxel
 // ownership is disjoint).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <memory>

@@ -161,26 +161,83 @@ inline unsigned copy_threads() {
     return n;
 }
 
+// Persistent copy workers (copy_threads() - 1 of them plus the caller):
+// spawning threads per call cost ~0.1-0.2 ms, too much for the 16 MB chunks
+// of the staged volume transfers. One job at a time (callers serialise).
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool(copy_threads()); // never destroyed: no join at exit
+        return *p;
+    }
+    void run(void* dst, const void* src, size_t bytes, size_t piece) {
+        std::lock_guard<std::mutex> job(job_mu_);
+        const size_t n = (bytes + piece - 1) / piece;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            piece_ = piece;
+            next_.store(0);
+            pieces_ = n;
+            left_ = n;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return left_ == 0; });
+    }
+
+  private:
+    explicit CopyPool(unsigned nt) {
+        for (unsigned i = 1; i < nt; ++i)
+            std::thread([this] { loop(); }).detach();
+    }
+    void work() {
+        size_t did = 0;
+        for (size_t i; (i = next_.fetch_add(1)) < pieces_;) {
+            const size_t off = i * piece_, len = std::min(piece_, bytes_ - off);
+            std::memcpy(dst_ + off, src_ + off, len);
+            ++did;
+        }
+        if (did) {
+            std::lock_guard<std::mutex> lk(mu_);
+            left_ -= did;
+            if (left_ == 0)
+                done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0, piece_ = 1, pieces_ = 0, left_ = 0;
+    std::atomic<size_t> next_{0};
+    uint64_t gen_ = 0;
+};
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-    const size_t kChunk = size_t(4) << 20;
-    const size_t nt = std::min<size_t>(copy_threads(), (bytes + kChunk - 1) / kChunk);
-    if (nt <= 1) {
+    const size_t kPiece = size_t(2) << 20;
+    if (copy_threads() <= 1 || bytes <= kPiece) {
         std::memcpy(dst, src, bytes);
         return;
     }
-    std::vector<std::thread> pool;
-    const size_t per = (bytes + nt - 1) / nt;
-    for (size_t t = 0; t < nt; ++t) {
-        const size_t off = t * per;
-        if (off >= bytes)
-            break;
-        const size_t len = std::min(per, bytes - off);
-        pool.emplace_back([=] {
-            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len);
-        });
-    }
-    for (auto& th : pool)
-        th.join();
+    // pieces of 2 MB, at least ~4 per thread for balance
+    const size_t piece = std::max<size_t>(256 << 10, std::min(kPiece, bytes / (4 * copy_threads())));
+    CopyPool::get().run(dst, src, bytes, (piece + 63) & ~size_t(63));
 }
 
 bool is_pinned(const void* p) {
@@ -199,7 +256,10 @@ bool is_pinned(const void* p) {
 // the neighbouring chunk. Pinned memory is copied directly (asynchronously).
 // ev: two events of the stream's device.
 struct ChunkedXfer {
-    static constexpr size_t kChunk = size_t(64) << 20;
+    const size_t kChunk = [] {
+        const char* e = std::getenv("CBB_XFER_CHUNK_MB"); // experiments
+        return size_t(e ? std::max(1, std::atoi(e)) : 64) << 20;
+    }();
     float* buf[2] = {nullptr, nullptr};
     ~ChunkedXfer() {
         for (auto b : buf)

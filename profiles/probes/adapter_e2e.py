@@ -19,7 +19,7 @@ L = g.edge_voxels
 vol = np.full((L, L, L), 0.25, np.float32)
 opt = pkg.Options(num_gpus=1)
 pkg.reconstruct_images(vol, g, parts, mats, opt)
-for _ in range(3):
+for _ in range(int(os.environ.get('REPS', '3'))):
     t0 = time.perf_counter()
     st = pkg.reconstruct_images(vol, g, parts, mats, opt)
     t = time.perf_counter() - t0
