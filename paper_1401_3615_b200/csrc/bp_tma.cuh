@@ -538,7 +538,7 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     __shared__ int s_tlist[kTmaBatch];      // staged projections in order
     __shared__ int2 s_box[kTmaBatch];
     __shared__ float s_bias[kTmaBatch];
-    __shared__ unsigned long long s_fit;
+    __shared__ unsigned s_fit2[2];          // per half: projections whose box fits
     __shared__ unsigned long long s_wmask[kTThreads / 32];
     __shared__ unsigned s_culled;
 
@@ -602,8 +602,10 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     }
     if (!args.cull || __any_sync(0xffffffffu, negz))
         todo = args.count == 64 ? ~0ull : ((1ull << args.count) - 1ull);
-    if (warp == 0) {
-      for (int half = 0; half < 2 && 32 * half < args.count; ++half) {
+    if (warp < 2 && 32 * warp < args.count) {
+      // warps 0 and 1: projections 0-31 and 32-63
+      {
+        const int half = warp;
         // block box for projection p: taps of every voxel of the tile
         // (padding voxels sit on real ones) lie in [floor(min ix), floor(max ix) + 2]
         const int p = 32 * half + lane;
@@ -637,10 +639,9 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         s_box[p] = make_int2(bx0, by0);
         // SmemFetch bias: 2^23 - (by0 * PITCH + bx0), exact (|.| < 2^22)
         s_bias[p] = 8388608.0f - (float)(by0 * PITCH + bx0);
-        const unsigned long long fm = (unsigned long long)__ballot_sync(0xffffffffu, fits)
-                                      << (32 * half);
+        const unsigned fm = __ballot_sync(0xffffffffu, fits);
         if (lane == 0)
-            s_fit = half ? (s_fit | fm) : fm;
+            s_fit2[half] = fm;
       }
     }
     if (lane == 0)
@@ -659,6 +660,8 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 #pragma unroll
     for (int w = 0; w < kTThreads / 32; ++w)
         act |= s_wmask[w];
+    const unsigned long long s_fit =
+        args.count > 32 ? ((unsigned long long)s_fit2[1] << 32) | s_fit2[0] : s_fit2[0];
     const unsigned long long tma_mask = act & s_fit;
     const unsigned stage_bytes = (unsigned)stage_floats * 4u;
     const int ntma = __popcll(tma_mask);
