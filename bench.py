@@ -9,7 +9,8 @@ filtered projections of 1248x960 (seeded synthetic stand-in for RabbitCT,
 see paper_1401_3615_b200/synth.py), full-basis voxel updates L^3 * N.
 
 One step = one full reconstruction: zero the volume, prepare the 496 resident
-projections, back-project them in batches of 32.
+projections, back-project them (launches of 64 projections for the
+TMA-staged kernel, 32 for the gather kernel).
   value : inputs resident in HBM; device-timed with CUDA events; max over ranks.
   e2e   : the public host API (cbb_reconstruct through reconstruct_arrays) from
           pinned host projections to the host volume, H2D + kernels + D2H.
