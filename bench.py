@@ -63,6 +63,9 @@ def parse():
                     help="skip the oracle check of the timed run's volume")
     ap.add_argument("--parity-stride", type=int, default=32,
                     help="oracle-check every k-th z-plane (plus the last) of the timed volume")
+    ap.add_argument("--ref-max-steps", type=int, default=3,
+                    help="reference arm: at most this many timed steps (1 warm-up): each "
+                         "is the full workload, ~15 s on 16 host cores")
     ap.add_argument("--ref-projections", type=int, default=0,
                     help="--impl reference: projections per step (0 = all, the stated config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -208,7 +211,13 @@ def run_reference_arm(args):
     from paper_1401_3615_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
-    total_steps = args.steps + args.warmup
+    # each step is the whole workload (~15 s on 16 cores incl. the clip/pad
+    # precompute), so the arm times min(K, --ref-max-steps) steps after at
+    # most one warm-up and reports the counts it ran: the run stays within a
+    # minute or two whatever K the caller asks for
+    ref_steps = max(1, min(args.steps, args.ref_max_steps))
+    ref_warmup = min(args.warmup, 1)
+    total_steps = ref_steps + ref_warmup
     # every step is the whole stated workload (all projections of the config
     # into the full volume: same_config with our arm); --ref-projections
     # bounds it for quick manual runs only
@@ -220,7 +229,7 @@ def run_reference_arm(args):
     cores = os.cpu_count() or 1
     for i in range(total_steps):
         gups, st, kind, cores = time_reference_cpu(cfg, n, g, mats, imgs)
-        if i >= args.warmup:
+        if i >= ref_warmup:
             vals.append(gups)
             secs.append(st["kernel_seconds"])
             pre.append(st.get("precompute_seconds", 0.0))
@@ -233,7 +242,8 @@ def run_reference_arm(args):
               f"by default); full-basis updates")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GUp/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": ref_steps, "warmup": ref_warmup,
+        "requested_steps": args.steps, "requested_warmup": args.warmup,
         "ms_per_step": round(1e3 * statistics.median(secs), 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "edge_voxels": cfg.edge_voxels,
