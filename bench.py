@@ -63,9 +63,10 @@ def parse():
                     help="skip the oracle check of the timed run's volume")
     ap.add_argument("--parity-stride", type=int, default=32,
                     help="oracle-check every k-th z-plane (plus the last) of the timed volume")
-    ap.add_argument("--ref-max-steps", type=int, default=3,
-                    help="reference arm: at most this many timed steps (1 warm-up): each "
-                         "is the full workload, ~15 s on 16 host cores")
+    ap.add_argument("--ref-max-steps", type=int, default=0,
+                    help="reference arm: at most this many timed steps after at most one "
+                         "warm-up (0 = exactly --steps/--warmup); each step is the full "
+                         "workload, ~15 s on 16 host cores")
     ap.add_argument("--ref-projections", type=int, default=0,
                     help="--impl reference: projections per step (0 = all, the stated config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -212,11 +213,12 @@ def run_reference_arm(args):
 
     cfg = synth.CONFIGS[args.config]
     # each step is the whole workload (~15 s on 16 cores incl. the clip/pad
-    # precompute), so the arm times min(K, --ref-max-steps) steps after at
-    # most one warm-up and reports the counts it ran: the run stays within a
-    # minute or two whatever K the caller asks for
-    ref_steps = max(1, min(args.steps, args.ref_max_steps))
-    ref_warmup = min(args.warmup, 1)
+    # precompute): K + W steps by default (20 + 5: ~6.5 min, inside the
+    # driver's limit); --ref-max-steps k caps a manual run at k timed steps
+    # after at most one warm-up, and the line reports the counts it ran
+    ref_steps = args.steps if args.ref_max_steps <= 0 else max(1, min(args.steps,
+                                                                       args.ref_max_steps))
+    ref_warmup = args.warmup if args.ref_max_steps <= 0 else min(args.warmup, 1)
     total_steps = ref_steps + ref_warmup
     # every step is the whole stated workload (all projections of the config
     # into the full volume: same_config with our arm); --ref-projections
