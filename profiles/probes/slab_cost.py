@@ -14,6 +14,7 @@ err = torch.zeros(1, dtype=torch.int32, device="cuda")
 pkg.scan_device(imgs, flags, err)
 vol = torch.zeros((L, L, L), dtype=torch.float32, device="cuda")
 fast = os.environ.get("FAST") == "1"
+COUNT = int(os.environ.get("COUNT", "64"))
 opt = pkg.Options(mode=pkg.MODE_FAST if fast else pkg.MODE_EXACT)
 ranges = [tuple(map(int, r.split(":"))) for r in os.environ["RANGES"].split(",")] if os.environ.get("RANGES") else [(0, 12), (0, 36), (12, 48), (464, 500), (500, 512), (476, 512), (250, 262), (232, 268), (0, 512), (48, 464)]
 for z0, z1 in ranges:
@@ -23,7 +24,7 @@ for z0, z1 in ranges:
     for rep in range(int(os.environ.get('REPS', 6))):
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         a.record()
-        pkg.backproject_raw_device(v, g, z0, z1, imgs, W, H, 64, mats, flags, opt, err, first=64 * (rep % 7))
+        pkg.backproject_raw_device(v, g, z0, z1, imgs, W, H, COUNT, mats, flags, opt, err, first=64 * (rep % 7))
         b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     t = float(np.median(ts[1:]))
