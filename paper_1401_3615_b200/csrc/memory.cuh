@@ -167,67 +167,105 @@ inline unsigned copy_threads() {
 class CopyPool {
   public:
     static CopyPool& get() {
-        static CopyPool* p = new CopyPool(copy_threads()); // never destroyed: no join at exit
+        static CopyPool* p = created() = new CopyPool(copy_threads()); // never destroyed
         return *p;
     }
+    static CopyPool*& created() { // null until first use (the unload hook checks it)
+        static CopyPool* p = nullptr;
+        return p;
+    }
     void run(void* dst, const void* src, size_t bytes, size_t piece) {
-        std::lock_guard<std::mutex> job(job_mu_);
-        const size_t n = (bytes + piece - 1) / piece;
+        std::lock_guard<std::mutex> one(job_mu_);
+        Job j;
+        j.dst = static_cast<char*>(dst);
+        j.src = static_cast<const char*>(src);
+        j.bytes = bytes;
+        j.piece = piece;
+        j.pieces = j.left = (bytes + piece - 1) / piece;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            dst_ = static_cast<char*>(dst);
-            src_ = static_cast<const char*>(src);
-            bytes_ = bytes;
-            piece_ = piece;
-            next_.store(0);
-            pieces_ = n;
-            left_ = n;
+            job_ = &j;
             ++gen_;
         }
         cv_.notify_all();
-        work();
+        work(j);
+        // the job lives on this stack: return only when no worker holds it
         std::unique_lock<std::mutex> lk(mu_);
-        done_.wait(lk, [&] { return left_ == 0; });
+        done_.wait(lk, [&] { return j.left == 0 && j.users == 0; });
+        job_ = nullptr;
+    }
+    // library unload (dlclose): wake the workers and wait until they left
+    // this library's code
+    void shutdown() {
+        std::unique_lock<std::mutex> lk(mu_);
+        stop_ = true;
+        cv_.notify_all();
+        done_.wait_for(lk, std::chrono::seconds(2), [&] { return live_ == 0; });
     }
 
   private:
+    struct Job {
+        char* dst = nullptr;
+        const char* src = nullptr;
+        size_t bytes = 0, piece = 1, pieces = 0, left = 0; // left, users: under mu_
+        int users = 0;
+        std::atomic<size_t> next{0};
+    };
     explicit CopyPool(unsigned nt) {
+        live_ = nt > 1 ? nt - 1 : 0;
         for (unsigned i = 1; i < nt; ++i)
             std::thread([this] { loop(); }).detach();
     }
-    void work() {
+    void work(Job& j) {
         size_t did = 0;
-        for (size_t i; (i = next_.fetch_add(1)) < pieces_;) {
-            const size_t off = i * piece_, len = std::min(piece_, bytes_ - off);
-            std::memcpy(dst_ + off, src_ + off, len);
+        for (size_t i; (i = j.next.fetch_add(1)) < j.pieces;) {
+            const size_t off = i * j.piece, len = std::min(j.piece, j.bytes - off);
+            std::memcpy(j.dst + off, j.src + off, len);
             ++did;
         }
         if (did) {
             std::lock_guard<std::mutex> lk(mu_);
-            left_ -= did;
-            if (left_ == 0)
+            j.left -= did;
+            if (j.left == 0)
                 done_.notify_all();
         }
     }
     void loop() {
         uint64_t seen = 0;
         for (;;) {
+            Job* j = nullptr;
             {
                 std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) {
+                    --live_;
+                    done_.notify_all();
+                    return;
+                }
                 seen = gen_;
+                j = job_; // null: that job already finished
+                if (!j)
+                    continue;
+                ++j->users;
             }
-            work();
+            work(*j);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--j->users == 0 && j->left == 0)
+                done_.notify_all();
         }
     }
     std::mutex job_mu_, mu_;
     std::condition_variable cv_, done_;
-    char* dst_ = nullptr;
-    const char* src_ = nullptr;
-    size_t bytes_ = 0, piece_ = 1, pieces_ = 0, left_ = 0;
-    std::atomic<size_t> next_{0};
+    Job* job_ = nullptr;
     uint64_t gen_ = 0;
+    unsigned live_ = 0;
+    bool stop_ = false;
 };
+
+__attribute__((destructor)) static void copy_pool_unload() {
+    if (CopyPool* p = CopyPool::created())
+        p->shutdown();
+}
 
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     const size_t kPiece = size_t(2) << 20;
