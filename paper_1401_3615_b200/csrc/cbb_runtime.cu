@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>

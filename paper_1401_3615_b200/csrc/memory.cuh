@@ -175,13 +175,21 @@ class CopyPool {
         return p;
     }
     void run(void* dst, const void* src, size_t bytes, size_t piece) {
+        char* d = static_cast<char*>(dst);
+        const char* s = static_cast<const char*>(src);
+        run_pieces((bytes + piece - 1) / piece, [=](size_t i) {
+            const size_t off = i * piece;
+            std::memcpy(d + off, s + off, std::min(piece, bytes - off));
+        });
+    }
+    // fn(i) for i in [0, pieces), spread over the workers and the caller
+    void run_pieces(size_t pieces, const std::function<void(size_t)>& fn) {
+        if (pieces == 0)
+            return;
         std::lock_guard<std::mutex> one(job_mu_);
         Job j;
-        j.dst = static_cast<char*>(dst);
-        j.src = static_cast<const char*>(src);
-        j.bytes = bytes;
-        j.piece = piece;
-        j.pieces = j.left = (bytes + piece - 1) / piece;
+        j.fn = &fn;
+        j.pieces = j.left = pieces;
         {
             std::lock_guard<std::mutex> lk(mu_);
             job_ = &j;
@@ -205,9 +213,8 @@ class CopyPool {
 
   private:
     struct Job {
-        char* dst = nullptr;
-        const char* src = nullptr;
-        size_t bytes = 0, piece = 1, pieces = 0, left = 0; // left, users: under mu_
+        const std::function<void(size_t)>* fn = nullptr;
+        size_t pieces = 0, left = 0; // left, users: under mu_
         int users = 0;
         std::atomic<size_t> next{0};
     };
@@ -219,8 +226,7 @@ class CopyPool {
     void work(Job& j) {
         size_t did = 0;
         for (size_t i; (i = j.next.fetch_add(1)) < j.pieces;) {
-            const size_t off = i * j.piece, len = std::min(j.piece, j.bytes - off);
-            std::memcpy(j.dst + off, j.src + off, len);
+            (*j.fn)(i);
             ++did;
         }
         if (did) {

@@ -940,20 +940,20 @@ struct Pipeline {
     void submit_images(const float* const* imgs, const double* mats, int count) {
         begin_stack(mats, count);
         ensure_staging();
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         for (int first = 0, n = 0; first < count; first += n) {
             n = batch_at(first, count);
             wait_stage(sslot);
             float* dst = h_stage[sslot];
-            const int nt = (int)std::min<unsigned>(copy_threads(), (unsigned)n);
-            std::vector<std::thread> pool;
-            for (int t = 0; t < nt; ++t)
-                pool.emplace_back([&, t] {
-                    for (int j = t; j < n; j += nt)
-                        std::memcpy(dst + (size_t)j * W * H, imgs[first + j], raw_bytes_per_proj);
-                });
-            for (auto& th : pool)
-                th.join();
+            // gathered by the copy pool in ~2 MB pieces of the images
+            const size_t per_img = std::max<size_t>(1, raw_bytes_per_proj / (size_t(2) << 20));
+            const size_t piece = (raw_bytes_per_proj + per_img - 1) / per_img;
+            CopyPool::get().run_pieces((size_t)n * per_img, [&](size_t i) {
+                const size_t j = i / per_img, off = (i % per_img) * piece;
+                if (off < raw_bytes_per_proj)
+                    std::memcpy(reinterpret_cast<char*>(dst + (size_t)j * W * H) + off,
+                                reinterpret_cast<const char*>(imgs[first + j]) + off,
+                                std::min(piece, raw_bytes_per_proj - off));
+            });
             issue(dst, mats + 12 * (size_t)first, n, sslot);
             sslot = (sslot + 1) % kStageSlots;
         }
