@@ -35,6 +35,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <immintrin.h>
 #include <nvtx3/nvToolsExt.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -622,7 +623,7 @@ cbb_status cbb_reconstruct(float* vol, const cbb_volume_geometry* geometry, cons
         double t_init = 0, t_sub = 0, t_fin = 0;
         {
             Pipeline pipe;
-            pipe.init(*geometry, width, height, opt, vol, mats, count);
+            pipe.init(*geometry, width, height, opt, vol, mats, count, /*defer_volume=*/true);
             t_init = ms();
             pipe.submit_stack(imgs, mats, count);
             t_sub = ms();
@@ -662,7 +663,7 @@ cbb_status cbb_reconstruct_images(float* vol, const cbb_volume_geometry* geometr
         const cbb_options opt = resolve_options(options);
         {
             Pipeline pipe;
-            pipe.init(*geometry, width, height, opt, vol, mats, count);
+            pipe.init(*geometry, width, height, opt, vol, mats, count, /*defer_volume=*/true);
             pipe.submit_images(imgs, mats, count);
             pipe.finish(vol);
             pipe.fill_stats(stats, 0.0);

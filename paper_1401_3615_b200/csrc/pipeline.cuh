@@ -191,6 +191,28 @@ struct Pipeline {
     bool raw_mode = false;
     int tail_group() const { return raw_mode ? kTR : 8; }
 
+    // Deferred initial volume (one worker, a volume to accumulate into):
+    // init() does not upload it. In raw resident mode (whole stack known)
+    // it goes up in z-chunks interleaved with the first batches -- one
+    // chunk ahead of each batch, the tail planes last -- and the head
+    // launches cover the chunks already on the device, each chunk catching
+    // up on the projections it missed (every voxel still takes the
+    // projections one by one in stack order, so the bits do not change).
+    // The pageable volume's upload (~14 ms for config 2's 537 MB through
+    // the staging chunks) then overlaps the projection stream instead of
+    // preceding it. Every other path uploads it whole before its first
+    // batch (upload_volume_whole).
+    const float* vol_src = nullptr; // the slab's first plane in the caller's volume
+    struct VolChunk {
+        int z0 = 0, z1 = 0;
+        int applied = 0;            // projections already back-projected into it
+        bool issued = false, tail = false;
+        cudaEvent_t ready = nullptr; // copy stream: uploaded and checked
+    };
+    std::vector<VolChunk> vchunks;
+    size_t vchunk_next = 0;
+    bool tails_chosen = false;
+
     // Resident mode for a stack of known size: when every packed projection
     // fits in device memory (with 2 GB to spare), keep them all so a dense
     // tail of each slab (choose_tails) can be back-projected after the stream
@@ -247,10 +269,16 @@ struct Pipeline {
     // the tail holds the smallest plane range with `frac` of the work: its
     // compute must cover the head's download, ~50 GB/s into pinned memory
     // but ~30 GB/s into pageable memory through the staging chunks (the C++
-    // adapter's volume): config 2 adapter path 110 -> 106 ms with 0.24
+    // adapter's volume): config 2 adapter path 110 -> 106 ms with 0.24;
+    // with the deferred volume and streaming host copies the stream phase
+    // is shorter and 0.16-0.20 balance it best (94.4 ms vs 96.4 at 0.24 and
+    // 0.12, 100 at 0.06: there the head launches outrun the uploads)
     bool out_pageable = false; // init: the caller's volume (in and out) is pageable
     void choose_tails(const double* mats, int n) {
-        double frac = out_pageable ? 0.24 : 0.12;
+        if (tails_chosen) // once per stack (the volume chunks follow the tails)
+            return;
+        tails_chosen = true;
+        double frac = out_pageable ? 0.18 : 0.12;
         if (const char* e = std::getenv("CBB_TAIL_FRAC"))
             frac = std::atof(e);
         for (auto& w : workers) {
@@ -299,6 +327,13 @@ struct Pipeline {
     }
 
     ~Pipeline() {
+        if (!workers.empty()) {
+            cudaSetDevice(workers[0]->device);
+            cudaStreamSynchronize(workers[0]->copy);
+        }
+        for (auto& c : vchunks)
+            if (c.ready)
+                cudaEventDestroy(c.ready);
         workers.clear();
         for (auto h : h_stage)
             HostPool::get().release(h);
@@ -306,9 +341,12 @@ struct Pipeline {
 
     // mats/nmats (nullable): the whole stack's matrices; with several devices
     // and culling on, the slabs are then balanced by estimated work instead
-    // of equal plane counts.
+    // of equal plane counts. defer_volume: a whole-stack call (cbb_reconstruct,
+    // cbb_reconstruct_images) whose volume may go up with the first batches
+    // (VolChunk); sessions validate the volume at creation, so they do not.
     void init(const cbb_volume_geometry& geom, int width, int height, const cbb_options& o,
-              const float* initial_volume, const double* mats = nullptr, int nmats = 0) {
+              const float* initial_volume, const double* mats = nullptr, int nmats = 0,
+              bool defer_volume = false) {
         g = geom;
         W = width;
         H = height;
@@ -385,7 +423,10 @@ struct Pipeline {
             CK(cudaMemsetAsync(w->d_counters, 0, cbytes, w->compute));
             w->count_culled = opt.count_culled != 0;
             CK(cudaEventRecord(w->c_beg, w->copy));
-            if (initial_volume && !opt.volume_is_zero) {
+            if (initial_volume && !opt.volume_is_zero && ng == 1 && defer_volume &&
+                !std::getenv("CBB_NO_VOL_DEFER")) {
+                vol_src = initial_volume + plane * w->z_begin; // see VolChunk
+            } else if (initial_volume && !opt.volume_is_zero) {
                 xfer.upload(w->d_vol, initial_volume + plane * w->z_begin, slab * sizeof(float),
                             w->copy, w->xfer_ev);
                 // Volume::validate (proj/src/dataset.cpp:146-151, called by
@@ -601,7 +642,127 @@ struct Pipeline {
     // back-projected into the head planes
     int raw_pending = 0;
     int raw_last_launch = 0;
+
+    // The deferred volume in one piece (every path but raw resident mode),
+    // before the first batch or at finish.
+    void upload_volume_whole() {
+        if (!vol_src || !vchunks.empty())
+            return;
+        Worker& w = *workers[0];
+        CK(cudaSetDevice(w.device));
+        const size_t slab = (size_t)g.edge_voxels * g.edge_voxels * (w.z_end - w.z_begin);
+        CK(cudaEventRecord(w.c_beg, w.copy));
+        xfer.upload(w.d_vol, vol_src, slab * sizeof(float), w.copy, w.xfer_ev);
+        launch_check_finite(w.d_vol, (long long)slab, w.d_err, w.copy, 4); // Volume::validate
+        CK(cudaEventRecord(w.c_end, w.copy));
+        CK(cudaStreamWaitEvent(w.compute, w.c_end, 0));
+        vol_src = nullptr;
+    }
+
+    // Raw resident mode, one worker: the deferred volume's z-chunks (see
+    // VolChunk). Head chunks of ~1/8 of the head planes in z order, aligned
+    // to the staged kernel's z-blocks, then the tail (needed only at finish).
+    void plan_volume_chunks() {
+        Worker& w = *workers[0];
+        choose_tails(est_mats, est_n);
+        const int gs = kTR;
+        int nchunks = 8;
+        if (const char* e = std::getenv("CBB_VOL_CHUNKS")) // experiments
+            nchunks = std::max(1, std::atoi(e));
+        const int head = (w.z_end - w.z_begin) - (w.tail_hi - w.tail_lo);
+        const int cp = std::max(gs, (head / nchunks + gs - 1) / gs * gs);
+        auto add = [&](int a, int b, bool tail) {
+            for (int z = a; z < b; z += cp) {
+                VolChunk c;
+                c.z0 = z;
+                c.z1 = tail ? b : std::min(z + cp, b);
+                c.tail = tail;
+                CK(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+                vchunks.push_back(c);
+                if (tail)
+                    break;
+            }
+        };
+        CK(cudaSetDevice(w.device));
+        add(w.z_begin, w.tail_lo, false);
+        add(w.tail_hi, w.z_end, false);
+        add(w.tail_lo, w.tail_hi, true);
+        if (std::getenv("CBB_TRACE"))
+            std::fprintf(stderr, "cbb: deferred volume in %zu chunks of %d planes (tail [%d, %d))\n",
+                         vchunks.size(), cp, w.tail_lo, w.tail_hi);
+    }
+
+    // Queues the next `k` volume chunks on the copy stream (pageable: through
+    // the staging chunks, this thread copying) with the finiteness check.
+    void pump_volume(size_t k) {
+        if (vchunks.empty())
+            return;
+        Worker& w = *workers[0];
+        CK(cudaSetDevice(w.device));
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        for (; k > 0 && vchunk_next < vchunks.size(); --k) {
+            VolChunk& c = vchunks[vchunk_next++];
+            const size_t off = plane * (c.z0 - w.z_begin), n = plane * (c.z1 - c.z0);
+            xfer.upload_async(w.d_vol + off, vol_src + off, n * sizeof(float), w.copy, w.xfer_ev);
+            // Volume::validate (proj/src/dataset.cpp:146-151): bit 4
+            launch_check_finite(w.d_vol + off, (long long)n, w.d_err, w.copy, 4);
+            CK(cudaEventRecord(c.ready, w.copy));
+            c.issued = true;
+        }
+    }
+
+    // launch_raw_pending with a chunked volume: projections [applied, end)
+    // into each run of uploaded head chunks with equal `applied` (a run
+    // spanning the tail skips it through the kernel's gap), i.e. one launch
+    // for the chunks that kept up and one for those that just arrived.
+    void launch_chunks_pending(int end) {
+        Worker& w = *workers[0];
+        CK(cudaSetDevice(w.device));
+        const size_t plane = (size_t)g.edge_voxels * g.edge_voxels;
+        for (auto& c : vchunks)
+            if (c.issued && c.ready) {
+                CK(cudaStreamWaitEvent(w.compute, c.ready, 0));
+                // waited once: the compute stream is ordered after it from now on
+                CK(cudaEventDestroy(c.ready));
+                c.ready = nullptr;
+            }
+        size_t i = 0;
+        while (i < vchunks.size()) {
+            VolChunk& a = vchunks[i];
+            if (a.tail || !a.issued || a.applied >= end) {
+                ++i;
+                continue;
+            }
+            size_t j = i + 1;
+            int z1 = a.z1;
+            while (j < vchunks.size() && !vchunks[j].tail && vchunks[j].issued &&
+                   vchunks[j].applied == a.applied &&
+                   (vchunks[j].z0 == z1 || (z1 == w.tail_lo && vchunks[j].z0 == w.tail_hi))) {
+                z1 = vchunks[j].z1;
+                ++j;
+            }
+            const int from = a.applied;
+            const bool gap = a.z0 < w.tail_lo && z1 > w.tail_hi;
+            w.guarded += launch_backproject_raw(
+                w.d_vol + plane * (a.z0 - w.z_begin), g, a.z0, z1,
+                static_cast<const float*>(w.d_packed_all) + (size_t)from * W * H,
+                (long long)W * H, W, H, 0, H, end - from, all_mats.data() + 12 * (size_t)from,
+                w.d_flags_all + from, w.plan, opt, w.d_err, w.compute, gap ? w.tail_lo : 0,
+                gap ? w.tail_hi : 0, w.count_culled ? w.d_counters : nullptr);
+            for (size_t k = i; k < j; ++k)
+                vchunks[k].applied = end;
+            i = j;
+        }
+    }
+
     void launch_raw_pending(int end) {
+        if (!vchunks.empty()) {
+            if (end > raw_pending)
+                raw_last_launch = end - raw_pending;
+            launch_chunks_pending(end);
+            raw_pending = std::max(raw_pending, end);
+            return;
+        }
         if (end <= raw_pending)
             return;
         Worker& w = *workers[0];
@@ -624,6 +785,15 @@ struct Pipeline {
 
     void issue(const float* src, const double* mats, int n, int stage = -1) {
         const auto t0 = std::chrono::steady_clock::now();
+        if (vol_src) { // the deferred volume goes ahead of the batch (VolChunk)
+            static const int per_batch = std::getenv("CBB_VOL_PER_BATCH")
+                                             ? std::max(1, std::atoi(std::getenv("CBB_VOL_PER_BATCH")))
+                                             : 1;
+            if (vchunks.empty())
+                upload_volume_whole();
+            else
+                pump_volume((size_t)per_batch);
+        }
         if (raw_mode)
             issue_raw(src, mats, n, stage);
         else
@@ -814,7 +984,7 @@ struct Pipeline {
         ensure_staging();
         if (stage_fill == 0)
             wait_stage(sslot);
-        std::memcpy(h_stage[sslot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
+        stream_copy(h_stage[sslot] + (size_t)stage_fill * W * H, img, raw_bytes_per_proj);
         std::memcpy(stage_mats.data() + 12 * (size_t)stage_fill, m, 12 * sizeof(double));
         if (++stage_fill == opt.batch)
             flush();
@@ -902,12 +1072,14 @@ struct Pipeline {
                 w->d_flags_all = static_cast<unsigned*>(
                     DevicePool::get().alloc(w->device, sizeof(unsigned) * count));
             }
+        est_mats = mats;
+        est_n = count;
+        if (vol_src && raw_mode && resident && workers.size() == 1)
+            plan_volume_chunks();
         if (std::getenv("CBB_TRACE"))
             std::fprintf(stderr, "cbb: enable_resident %.2f ms\n",
                          std::chrono::duration<double, std::milli>(
                              std::chrono::steady_clock::now() - t0).count());
-        est_mats = mats;
-        est_n = count;
     }
 
     void submit_stack(const float* imgs, const double* mats, int count) {
@@ -950,7 +1122,7 @@ struct Pipeline {
             CopyPool::get().run_pieces((size_t)n * per_img, [&](size_t i) {
                 const size_t j = i / per_img, off = (i % per_img) * piece;
                 if (off < raw_bytes_per_proj)
-                    std::memcpy(reinterpret_cast<char*>(dst + (size_t)j * W * H) + off,
+                    stream_copy(reinterpret_cast<char*>(dst + (size_t)j * W * H) + off,
                                 reinterpret_cast<const char*>(imgs[first + j]) + off,
                                 std::min(piece, raw_bytes_per_proj - off));
             });
@@ -1013,7 +1185,7 @@ struct Pipeline {
                         const uint64_t off = header_bytes + rec_bytes * (uint64_t)(first + j);
                         if (map) {
                             std::memcpy(mats.data() + 12 * (size_t)j, map + off, 96);
-                            std::memcpy(dst + (size_t)j * W * H, map + off + 96, rec_bytes - 96);
+                            stream_copy(dst + (size_t)j * W * H, map + off + 96, rec_bytes - 96);
                         } else if (!pread_all(fd, mats.data() + 12 * (size_t)j, 96, off) ||
                                    !pread_all(fd, dst + (size_t)j * W * H, rec_bytes - 96,
                                               off + 96)) {
@@ -1084,6 +1256,12 @@ struct Pipeline {
     void finish(float* vol_out) {
         NvtxRange range("cbb finish");
         flush();
+        if (vol_src) { // nothing submitted, or chunks still to upload
+            if (vchunks.empty())
+                upload_volume_whole();
+            else
+                pump_volume(vchunks.size());
+        }
         if (raw_mode && resident && workers.size() == 1)
             launch_raw_pending((int)submitted);
         if (std::getenv("CBB_TRACE") && issue_count)
