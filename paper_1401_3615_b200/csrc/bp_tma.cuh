@@ -747,6 +747,9 @@ bp_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     };
     if (act == tma_mask) {
         // common case: every active projection is staged
+#if defined(CBB_TMA_UNROLL) && CBB_TMA_UNROLL == 2
+#pragma unroll 2
+#endif
         for (int t = 0; t < ntma; ++t)
             staged(s_tlist[t]);
     } else {
