@@ -35,7 +35,6 @@
 #include <vector>
 
 #include <cuda_runtime.h>
-#include <immintrin.h>
 #include <nvtx3/nvToolsExt.h>
 #include <fcntl.h>
 #include <sys/mman.h>

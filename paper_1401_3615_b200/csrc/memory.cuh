@@ -5,6 +5,8 @@
 // memory.cuh, pipeline.cuh).
 #pragma once
 
+#include <immintrin.h> // stream_copy's AVX2 streaming stores
+
 namespace cbb {
 
 // ---------------------------------------------------------------------------

@@ -34,6 +34,19 @@ int main() {
             if (std::memcmp(dst.data(), src.data(), n)) ++bad;
         }
     };
+    // stream_copy (AVX2 streaming stores): every destination/source
+    // misalignment and sizes around the 4 KB threshold and the 128 B loop
+    for (size_t n : {0ul, 1ul, 31ul, 127ul, 4095ul, 4096ul, 4097ul, 4224ul, 65537ul, 1000003ul})
+        for (int da = 0; da < 64; da += 3)
+            for (int sa = 0; sa < 8; ++sa) {
+                std::memset(b.data(), 0x5a, n + 256);
+                cbb::stream_copy(b.data() + 64 + da, a.data() + sa, n);
+                if (std::memcmp(b.data() + 64 + da, a.data() + sa, n)) ++bad;
+                for (int i = 0; i < 64 + da; ++i) // nothing written before dst
+                    if (b[i] != 0x5a) { ++bad; break; }
+                for (int i = 0; i < 64; ++i) // nor after dst + n
+                    if (b[64 + da + n + i] != 0x5a) { ++bad; break; }
+            }
     std::vector<std::thread> ts;
     for (int i = 0; i < 4; ++i) ts.emplace_back(worker, i);
     for (int it = 0; it < 50; ++it) {
