@@ -115,3 +115,34 @@ def test_config4_planes_all_projections_bitwise(cuda, oracle):
     print(f"config 4: {planes.size} planes x all 1440 projections bitwise "
           f"(oracle {secs:.1f} s, cache hit {hit})")
     pkg.release_cached_memory()
+
+
+def test_config2_adapter_path_deferred_volume(cuda, monkeypatch):
+    """The C++ adapter's call at the headline size: cbb_reconstruct_images
+    from pageable per-image buffers into a non-zero pageable volume, whose
+    upload is deferred into z-chunks that the head launches follow
+    (pipeline.cuh, VolChunk), bitwise equal to uploading the volume whole
+    first (CBB_NO_VOL_DEFER) over the whole 512^3 volume."""
+    import torch
+
+    cfg = synth.CONFIGS[2]
+    g, mats, imgs = synth.make_inputs(cfg, device="cuda", out_device="cpu", chunk=16)
+    host = imgs.numpy()
+    torch.cuda.empty_cache()
+    parts = [np.array(host[i]) for i in range(host.shape[0])]
+    del imgs, host
+    L = g.edge_voxels
+    rng = np.random.default_rng(4)
+    v0 = rng.standard_normal((L, L, L), dtype=np.float32)
+    v0[::5, :, 7] = -0.0
+    opt = pkg.Options(num_gpus=1)
+    a = v0.copy()
+    monkeypatch.setenv("CBB_TRACE", "1")
+    st = pkg.reconstruct_images(a, g, parts, mats, opt)
+    assert st["guarded_batches"] == 0
+    monkeypatch.delenv("CBB_TRACE")
+    monkeypatch.setenv("CBB_NO_VOL_DEFER", "1")
+    b = v0.copy()
+    pkg.reconstruct_images(b, g, parts, mats, opt)
+    assert not bits_equal(a, v0)
+    assert bits_equal(a, b), _diff(a, b)

@@ -90,6 +90,19 @@ def test_chunked_volume_equals_whole_upload(scan, vol0, monkeypatch):
     assert bits_equal(v1, v2)
 
 
+@pytest.mark.parametrize("env", ["CBB_NO_RESIDENT", "CBB_BP_PATH"])
+def test_deferred_volume_whole_upload_paths(scan, vol0, expected, monkeypatch, capfd, env):
+    """Without raw resident mode (no resident stack, or the packed gather
+    kernel) the deferred volume is uploaded whole before the first batch."""
+    g, mats, host = scan
+    monkeypatch.setenv(env, "quad" if env == "CBB_BP_PATH" else "1")
+    monkeypatch.setenv("CBB_TRACE", "1")
+    for images in (False, True):
+        v, _ = run(g, mats, host, vol0, images=images)
+        assert "deferred volume in" not in capfd.readouterr().err
+        assert bits_equal(v, expected)
+
+
 def test_chunked_volume_pinned_volume(scan, vol0, expected):
     """A pinned caller volume is uploaded chunk by chunk without staging."""
     import torch
