@@ -126,7 +126,10 @@ cbb_status cbb_backproject(float* vol, const cbb_volume_geometry* geometry,
  * floats, mats count*12 doubles. The input volume is validated like
  * Volume::validate (proj/src/dataset.cpp:146-151): a non-finite voxel gives
  * CBB_ERR_INVALID and the volume is left unchanged (skipped when
- * options->volume_is_zero promises zeros). Multi-GPU: work-balanced z-slabs,
+ * options->volume_is_zero promises zeros). On one GPU the input volume is
+ * uploaded in z-chunks alongside the first batches rather than before them
+ * (the call still reads it, and writes the result, only while it runs).
+ * Multi-GPU: work-balanced z-slabs,
  * one per device, all driven from the calling thread; each batch is uploaded
  * once and the other devices read their row bands over peer memory (P2P
  * loads inside the pack kernel, not an NCCL broadcast -- NCCL is used by the
