@@ -278,7 +278,10 @@ struct Pipeline {
         if (tails_chosen) // once per stack (the volume chunks follow the tails)
             return;
         tails_chosen = true;
-        double frac = out_pageable ? 0.18 : 0.12;
+        // pinned: 0.10-0.18 measured within 0.3 % of each other (76.0 +- 0.2 ms,
+        // profiles/e2e_tail_r2.txt); 0.14 leaves ~3 ms of tail compute beyond
+        // the 8.3 ms head download, for boxes with slower D2H
+        double frac = out_pageable ? 0.18 : 0.14;
         if (const char* e = std::getenv("CBB_TAIL_FRAC"))
             frac = std::atof(e);
         for (auto& w : workers) {
