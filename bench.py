@@ -61,7 +61,7 @@ def parse():
                     help="skip the config-4 (1440 x 1536^2 -> 1024^3) secondary")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the oracle check of the timed run's volume")
-    ap.add_argument("--parity-stride", type=int, default=32,
+    ap.add_argument("--parity-stride", type=int, default=8,
                     help="oracle-check every k-th z-plane (plus the last) of the timed volume")
     ap.add_argument("--ref-max-steps", type=int, default=0,
                     help="reference arm: at most this many timed steps after at most one "
