@@ -11,7 +11,10 @@ held to the stronger bar of bitwise equality:
     projections, through cbb_reconstruct (resident tail on);
   * config 4 (1024^3, 1440 x 1536^2, 360 deg, 30 ellipsoids): 16 planes with
     ALL 1440 projections, through cbb_reconstruct from host memory in
-    batches of 16 as BASELINE states.
+    batches of 16 as BASELINE states;
+  * the C++ adapter's call at config 2 with a non-zero pageable volume
+    (deferred, chunked volume upload) against the whole-volume upload;
+  * a 2048^3 volume (more than 2^32 voxels) through the host API.
 
 The oracle planes are computed by oracle_reconstruct_planes on all host
 threads and cached under a content hash of the inputs, like the reference
