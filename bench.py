@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 from types import SimpleNamespace
 import os
 import statistics
@@ -40,6 +41,7 @@ for _p in (ROOT, os.path.join(ROOT, "oracle")):
 METRIC = "GUp/s FDK backprojection, 512^3 & 1024^3 vol, 496x1248x960 proj, 1-8 B200"
 OPS_PER_UPDATE = 34  # algorithmic FP32 ops per voxel update
 GATHER_BYTES_PER_UPDATE = 16
+FP64_PEAK_TFLOPS = 33.75  # measured DFMA throughput on B200 (profiles/fp64_peak_r2.txt)
 
 
 def parse():
@@ -845,12 +847,27 @@ def filter_entry(c):
     pixels = n * H * W
     peaks, src = measured_peaks()
     alg_bytes = 8 * pixels  # read + write one float per pixel
+    # FP64-bound (ncu profiles/r2_ramp2560.txt: FP64 pipe 46 %, DRAM 9 %): two
+    # rows per complex transform of the padded length N (2560 for W <= 1280,
+    # 4096 for W <= 2048, else cuFFT's power of two), forward + inverse at the
+    # conventional 5 N log2 N flops each, plus the real spectrum multiply
+    nfft = 2560 if W <= 1280 else 4096 if W <= 2048 else 1 << (2 * W - 1).bit_length()
+    pairs = (n * H + 1) // 2
+    alg_flops = pairs * (2 * 5 * nfft * math.log2(nfft) + 2 * nfft)
+    fp64_tflops = FP64_PEAK_TFLOPS
     res = {"workload": cfg.name, "stage": "ramp filter (Shepp-Logan, row-wise, float64)",
            "ms_per_stack": round(ms, 3), "share_of_step": round(ms / c.ms_step, 4),
-           "roofline": {"bound": "hbm", "achieved": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
-                        "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                        "frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peaks.get("hbm_gbs"), 4),
-                        "algorithmic_bytes": int(alg_bytes), "peak_source": src}}
+           "roofline": {"bound": "fp64", "achieved": round(alg_flops / (ms * 1e-3) / 1e12, 2),
+                        "peak": fp64_tflops, "unit": "TFLOP/s",
+                        "frac": round(alg_flops / (ms * 1e-3) / 1e12 / fp64_tflops, 4),
+                        "algorithmic_flops": int(alg_flops), "fft_length": nfft,
+                        "peak_source": "measured DFMA throughput, profiles/probes/fp64_peak.cu "
+                                       "(profiles/fp64_peak_r2.txt)",
+                        "alongside": {"hbm": {
+                            "achieved_GBps": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
+                            "peak_GBps": peaks.get("hbm_gbs"),
+                            "frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peaks.get("hbm_gbs"), 4),
+                            "algorithmic_bytes": int(alg_bytes), "peak_source": src}}}}
     impl = pkg.ramp_filter_info() if hasattr(pkg, "ramp_filter_info") else None
     if impl:
         res["implementation"] = impl
