@@ -554,6 +554,167 @@ ramp_fft2560_rows(const float* raw, float* out, int W, long long rows,
     }
 }
 
+// ramp_fft2560_rows with 160 threads per CTA (kRf2T16), 3 CTAs per SM: the
+// four radix-16 passes (most of the FP64 work) use every thread instead of
+// 160 of 256, and the two radix-10 passes (256 butterflies) take two rounds
+// on threads 0-95. Same operations in the same order on the same values, so
+// the same bits as ramp_fft2560_rows.
+constexpr int kRf2T = kRf2T16;
+__global__ void __launch_bounds__(kRf2T, 3)
+ramp_fft2560_rows160(const float* raw, float* out, int W, long long rows,
+                     const double* __restrict__ spec, const double2* __restrict__ tw) {
+    extern __shared__ double2 rf_smem[];
+    double2* buf = rf_smem;
+    double* hs = reinterpret_cast<double*>(rf_smem + kRf2N);
+    double2* tw256 = reinterpret_cast<double2*>(hs + kRf2N / 2 + 2);
+    double2* tw16x = tw256 + 256; // tw[16 m], m < 10: forward radix-16 pass, Ns = 10
+    double2* tw10x = tw16x + 10;  // tw[10 m], m < 16: inverse radix-16 pass, Ns = 16
+    float* stg = reinterpret_cast<float*>(tw10x + 16);
+    constexpr int SROW = kRf2MaxW;
+    const int j = threadIdx.x;
+    for (int k = j; k <= kRf2N / 2; k += kRf2T)
+        hs[k] = spec[k];
+    for (int k = j; k < 256; k += kRf2T)
+        tw256[k] = __ldg(tw + k);
+    if (j < 10)
+        tw16x[j] = __ldg(tw + 16 * j);
+    if (j < 16)
+        tw10x[j] = __ldg(tw + 10 * j);
+    const long long pairs = (rows + 1) / 2;
+    auto prefetch = [&](long long p, int s) {
+        if (p < pairs) {
+            const float* r1 = raw + (2 * p) * (long long)W;
+            const int nrow = 2 * p + 1 < rows ? 2 : 1;
+            for (int e = j; e < nrow * W; e += kRf2T) {
+                const int row = e >= W, n = e - row * W;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(stg + (2 * s + row) * SROW + n);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(r1 + e));
+            }
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    prefetch(blockIdx.x, 0);
+    __syncthreads();
+    int s = 0;
+    for (long long p = blockIdx.x; p < pairs; p += gridDim.x, s ^= 1) {
+        const bool two = 2 * p + 1 < rows;
+        cd v[16];
+        prefetch(p + gridDim.x, s ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        // forward A: radix 10, Ns = 1, butterflies b = j, j + 160 (< 256): -> buf[10 b + q]
+        {
+            const float* a = stg + 2 * s * SROW;
+            for (int b = j; b < 256; b += kRf2T) {
+#pragma unroll
+                for (int r = 0; r < 10; ++r) {
+                    const int n = b + r * 256;
+                    const bool in = r < 5 && n < W;
+                    v[r] = cd{in ? (double)a[n] : 0.0, (in && two) ? (double)a[SROW + n] : 0.0};
+                }
+                dft10<false, true>(v);
+#pragma unroll
+                for (int q = 0; q < 10; ++q)
+                    buf[rf_sw(10 * b + q)] = make_double2(v[x10(q)].x, v[x10(q)].y);
+            }
+        }
+        __syncthreads();
+        // forward B: radix 16, Ns = 10
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+            v[r] = cd{x.x, x.y};
+        }
+        __syncthreads();
+        {
+            const double2 t = tw16x[j % 10];
+            rf2_twiddle16<false, 10>(v, cd{t.x, t.y});
+            dft16<false>(v);
+            const int base = (j / 10) * 160 + (j % 10);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(base + 10 * q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // forward C: radix 16, Ns = 160 -> registers: v[q] = Z[j + 160 q]
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+            v[r] = cd{x.x, x.y};
+        }
+        __syncthreads();
+        {
+            const double2 t = tw256[j];
+            rf2_twiddle16<false, 160>(v, cd{t.x, t.y});
+            dft16<false>(v);
+            cd o[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                o[q] = v[x16(q)];
+            // spectrum multiply, then inverse A: radix 16, Ns = 1 -> buf[16 j + q]
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int k = j + kRf2T16 * q;
+                const double h = hs[k <= kRf2N / 2 ? k : kRf2N - k];
+                v[q] = cd{o[q].x * h, o[q].y * h};
+            }
+            dft16<true>(v);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(16 * j + q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // inverse B: radix 16, Ns = 16
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const double2 x = buf[rf_sw(j + kRf2T16 * r)];
+            v[r] = cd{x.x, x.y};
+        }
+        __syncthreads();
+        {
+            const double2 t = tw10x[j % 16];
+            rf2_twiddle16<true, 16>(v, cd{t.x, t.y});
+            dft16<true>(v);
+            const int base = (j / 16) * 256 + (j % 16);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                buf[rf_sw(base + 16 * q)] = make_double2(v[x16(q)].x, v[x16(q)].y);
+        }
+        __syncthreads();
+        // inverse C: radix 10, Ns = 256, butterflies b = j, j + 160: y[b + 256 q]
+        float* o1 = out + (2 * p) * (long long)W;
+        for (int b = j; b < 256; b += kRf2T) {
+#pragma unroll
+            for (int r = 0; r < 10; ++r) {
+                const double2 x = buf[rf_sw(b + 256 * r)];
+                v[r] = cd{x.x, x.y};
+            }
+            {
+                const double2 t = tw256[b];
+                const cd w1{t.x, -t.y};
+                cd w = w1;
+#pragma unroll
+                for (int r = 1; r < 10; ++r) {
+                    v[r] = cmul(v[r], w);
+                    if (r < 9)
+                        w = cmul(w, w1);
+                }
+            }
+            dft10<true, false>(v);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const int n = b + q * 256;
+                if (n < W) {
+                    o1[n] = (float)v[x10(q)].x;
+                    if (two)
+                        o1[W + n] = (float)v[x10(q)].y;
+                }
+            }
+        }
+        __syncthreads(); // buf reused by the next pair's first pass
+    }
+}
+
 // spec[k] = (1/N) sum_n hc[n] cos(2 pi k n / N), hc the wrapped kernel
 // (n <= N/2: h(n), else h(n - N)); tw[e] = exp(-2 pi i e / N).
 __global__ void ramp_fft_tables(double* spec, double2* tw, int N, double tau) {
@@ -644,8 +805,23 @@ inline void ramp_fft_device(const float* raw, float* out, int W, int H, int coun
                        "cudaFuncSetAttribute(ramp_fft2560_rows)");
             attr2[dev] = true;
         }
-        ramp_fft2560_rows<<<(unsigned)grid, kRfT, kRf2Bytes, st>>>(raw, out, W, rows, t2.spec,
-                                                                  t2.tw);
+        const bool use256 = std::getenv("CBB_RAMP_256") != nullptr; // comparisons (tests)
+        if (use256) {
+            ramp_fft2560_rows<<<(unsigned)grid, kRfT, kRf2Bytes, st>>>(raw, out, W, rows, t2.spec,
+                                                                      t2.tw);
+        } else {
+            static bool attr3[64] = {};
+            if (dev < 64 && !attr3[dev]) {
+                check_cuda(cudaFuncSetAttribute(ramp_fft2560_rows160,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kRf2Bytes),
+                           "cudaFuncSetAttribute(ramp_fft2560_rows160)");
+                attr3[dev] = true;
+            }
+            const long long grid3 = std::min<long long>(pairs, (long long)nsm * 3); // 3 CTAs/SM
+            ramp_fft2560_rows160<<<(unsigned)grid3, kRf2T, kRf2Bytes, st>>>(raw, out, W, rows,
+                                                                            t2.spec, t2.tw);
+        }
         check_cuda(cudaGetLastError(), "ramp_fft2560_rows");
         ++g_launches;
         return;

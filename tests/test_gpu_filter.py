@@ -124,3 +124,22 @@ def test_filtered_pipeline_equals_backprojecting_filtered_data(cuda, oracle):
     pkg.reconstruct(vol, pkg.ProjectionStack(g, mats, raw),
                     pkg.Options(ramp_filter_pixel_mm=cfg.pixel_mm, batch=4))
     assert np.array_equal(vol.voxels.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("width,rows", [(1248, 9600), (1248, 7), (977, 301), (1280, 64), (5, 9)])
+def test_ramp_2560_kernel_thread_layouts_bitwise(cuda, monkeypatch, width, rows):
+    """The N = 2560 filter in 160-thread CTAs (ramp_fft2560_rows160, the
+    default: every thread busy in the radix-16 passes, 3 CTAs/SM) performs the
+    same operations as the 256-thread kernel (CBB_RAMP_256), so the same bits
+    -- over many grid-stride iterations (9600 rows) and odd row counts."""
+    import torch
+
+    r = np.random.default_rng(width + rows)
+    raw = torch.from_numpy((r.standard_normal((1, rows, width)) * 30).astype(np.float32)).cuda()
+    a = torch.empty_like(raw)
+    b = torch.empty_like(raw)
+    pkg.ramp_filter_device(raw, a, 0.32)
+    monkeypatch.setenv("CBB_RAMP_256", "1")
+    pkg.ramp_filter_device(raw, b, 0.32)
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
